@@ -1,0 +1,86 @@
+"""Bubble / makespan metrics over a timeline (simulated or device-measured).
+
+The metric definitions are the reference's (``P/simulate.py:54-97``):
+
+* makespan   = latest task end;
+* busy[st]   = sum of compute-task durations on stage ``st``;
+* bubble[st] = makespan - busy[st];
+* bubble fraction = sum(bubble) / (n_stages * makespan);
+* peak activation = max prefix sum of ``mem_delta`` applied at task end,
+  frees ordered before allocations at equal times.
+
+:func:`simulate` replays a schedule through the integer engine (the
+reference's prediction); :func:`metrics_from_timeline` applies the same
+definitions to CUDA-event timelines recorded by the B200 executor, so
+predicted and measured bubble are directly comparable.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from .costs import DurationTable
+from .engine import CommModel, make_duration_fn, replay
+from .schedule import SEND, Schedule
+
+
+@dataclass
+class Metrics:
+    makespan: float
+    per_stage_busy: list[float]
+    per_stage_bubble: list[float]
+    bubble_fraction: float
+    per_stage_peak_activation: list[int]
+    total_send_elements: int
+    time_unit: str
+
+
+@dataclass
+class SimResult:
+    sched: Schedule
+    timeline: dict[str, tuple[float, float]]
+    metrics: Metrics
+
+
+def memory_profile(sched: Schedule, timeline) -> list[list[tuple[float, int]]]:
+    profiles = []
+    for order in sched.per_stage_order:
+        events = sorted((timeline[tid][1], sched.tasks[tid].mem_delta > 0, tid,
+                         sched.tasks[tid].mem_delta)
+                        for tid in order if sched.tasks[tid].mem_delta)
+        level, prof = 0, []
+        for when, _alloc, _tid, delta in events:
+            level += delta
+            prof.append((when, level))
+        profiles.append(prof)
+    return profiles
+
+
+def metrics_from_timeline(sched: Schedule, timeline, time_unit: str = "ms") -> Metrics:
+    """Reference metric definitions applied to an arbitrary (start, end) timeline.
+
+    ``timeline`` must cover every compute task; comm tasks are optional (a
+    device timeline records them on the comm stream).
+    """
+    n = sched.n_stages
+    makespan = max((end for _s, end in timeline.values()), default=0)
+    t0 = min((start for start, _e in timeline.values()), default=0)
+    makespan -= t0
+    busy = [0.0] * n
+    for tid, (start, end) in timeline.items():
+        task = sched.tasks[tid]
+        if task.is_compute:
+            busy[task.stage] += end - start
+    bubble = [makespan - b for b in busy]
+    peaks = [max((lvl for _t, lvl in prof), default=0)
+             for prof in memory_profile(sched, timeline)]
+    sends = sum(t.volume for t in sched.tasks.values() if t.kind == SEND)
+    frac = sum(bubble) / (n * makespan) if makespan else 0.0
+    return Metrics(makespan, busy, bubble, frac, peaks, sends, time_unit)
+
+
+def simulate(sched: Schedule, durations: DurationTable, comm: CommModel | None = None) -> SimResult:
+    fused = sched.meta.get("backward") == "fused"
+    res = replay(sched, make_duration_fn(durations, fused), comm or CommModel.zero())
+    return SimResult(sched, res.timeline,
+                     metrics_from_timeline(sched, res.timeline, durations.time_unit))

@@ -1,0 +1,26 @@
+# Builds paper_2507_00394_b200/libhx.so (sm_100a) and the oracle's C pieces.
+NVCC ?= /usr/local/cuda/bin/nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := -O3 -std=c++17 -lineinfo $(ARCH) -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
+           --expt-relaxed-constexpr -Iinclude
+SRC := $(wildcard paper_2507_00394_b200/csrc/*.cu)
+HDR := $(wildcard paper_2507_00394_b200/csrc/*.cuh paper_2507_00394_b200/csrc/*.h include/*.h)
+OBJ := $(patsubst paper_2507_00394_b200/csrc/%.cu,build/%.o,$(SRC))
+LIB := paper_2507_00394_b200/libhx.so
+
+all: $(LIB)
+
+build/%.o: paper_2507_00394_b200/csrc/%.cu $(HDR)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(LIB): $(OBJ)
+	$(NVCC) $(ARCH) -shared $(OBJ) -o $@
+
+ptxas: $(SRC)
+	@for f in $(SRC); do $(NVCC) $(NVFLAGS) -Xptxas -v -c $$f -o /dev/null 2>&1 | grep -E "Function properties|registers|spill|error" ; done
+
+clean:
+	rm -rf build $(LIB)
+
+.PHONY: all clean ptxas

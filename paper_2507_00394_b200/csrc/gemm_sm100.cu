@@ -1,0 +1,312 @@
+// Persistent tcgen05 GEMM for the helix components (SURVEY.md §2.2 K2, K4, K6,
+// K7, K9, K11, K13, K14):
+//
+//   C[M,N] (epilogue)= op(A)[M,K] * op(B)[K,N],  bf16 operands, f32 accumulate
+//
+// Operand storage (row-major in HBM, "ld" = row stride in elements):
+//   a_mn = 0 : A stored [M, K] (K contiguous)   -> UMMA K-major
+//   a_mn = 1 : A stored [K, M] (M contiguous)   -> UMMA MN-major (weight grads, X^T * dY)
+//   b_mn = 0 : B stored [N, K] (K contiguous)   -> UMMA K-major  (input grads, dY * W^T)
+//   b_mn = 1 : B stored [K, N] (N contiguous)   -> UMMA MN-major (forward, X * W)
+//
+// Structure (one CTA per SM, 256 threads):
+//   warp 0 lane 0 : TMA producer, STAGES-deep smem ring (128B-swizzled tiles)
+//   warp 1 lane 0 : UMMA issuer, 128 x BN x 16 tcgen05.mma, accumulator in TMEM,
+//                   two accumulator buffers so the epilogue of tile i overlaps
+//                   the MMAs of tile i+1
+//   warp 2        : TMEM allocator
+//   warps 4..7    : epilogue: tcgen05.ld 32 columns at a time, fused op, store
+// Tiles are visited in M-grouped raster order (16 M-blocks per group) so the
+// concurrently resident A and B panels stay in the 126 MB L2.
+#include "hx_common.cuh"
+#include "hx_gemm.h"
+
+namespace hx {
+
+constexpr int GEMM_BM = 128;
+constexpr int GEMM_BK = 64;
+constexpr int GEMM_THREADS = 256;
+constexpr int GEMM_GROUP_M = 16;
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int STAGES = BN == 256 ? 4 : 6;
+  static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;  // 16 KB
+  static constexpr int B_BYTES = BN * GEMM_BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BAR_OFFSET = STAGES * STAGE_BYTES;
+  static constexpr int SMEM_BYTES = BAR_OFFSET + 256 + 1024;  // barriers + align slack
+  static constexpr int TMEM_COLS = 2 * BN;
+};
+
+__device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb, int& nb) {
+  const int per_group = GEMM_GROUP_M * num_n;
+  const int group = t / per_group;
+  const int first_m = group * GEMM_GROUP_M;
+  const int gm = min(num_m - first_m, GEMM_GROUP_M);
+  const int r = t - group * per_group;
+  mb = first_m + r % gm;
+  nb = r / gm;
+}
+
+// Fused epilogue for 32 consecutive accumulator columns of one row.
+__device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row, int col,
+                                               const uint32_t (&acc)[32]) {
+  if (row >= p.M) return;
+  float v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(acc[i]);
+  const int epi = p.epi;
+  if (epi == HX_EPI_STORE_F32 || epi == HX_EPI_ACC_F32) {
+    float* out = reinterpret_cast<float*>(p.out) + static_cast<int64_t>(row) * p.ldo + col;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (col + 4 * j + 4 > p.N) break;
+      float4 w = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      if (epi == HX_EPI_ACC_F32) {
+        float4 o = *reinterpret_cast<float4*>(out + 4 * j);
+        w.x += o.x; w.y += o.y; w.z += o.z; w.w += o.w;
+      }
+      *reinterpret_cast<float4*>(out + 4 * j) = w;
+    }
+    return;
+  }
+  __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out) + static_cast<int64_t>(row) * p.ldo + col;
+  const __nv_bfloat16* aux =
+      p.aux ? reinterpret_cast<const __nv_bfloat16*>(p.aux) + static_cast<int64_t>(row) * p.ld_aux + col
+            : nullptr;
+  __nv_bfloat16* out2 =
+      p.out2 ? reinterpret_cast<__nv_bfloat16*>(p.out2) + static_cast<int64_t>(row) * p.ldo2 + col
+             : nullptr;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (col + 8 * j + 8 > p.N) break;
+    float x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = v[8 * j + i];
+    if (epi == HX_EPI_RESID_BF16 || epi == HX_EPI_DGELU) {
+      uint4 a = *reinterpret_cast<const uint4*>(aux + 8 * j);
+      const uint32_t aw[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float2 f = unpack_bf16(aw[i]);
+        if (epi == HX_EPI_RESID_BF16) {
+          x[2 * i] += f.x;
+          x[2 * i + 1] += f.y;
+        } else {
+          x[2 * i] *= gelu_erf_grad(f.x);
+          x[2 * i + 1] *= gelu_erf_grad(f.y);
+        }
+      }
+    }
+    uint4 o;
+    o.x = pack_bf16(x[0], x[1]);
+    o.y = pack_bf16(x[2], x[3]);
+    o.z = pack_bf16(x[4], x[5]);
+    o.w = pack_bf16(x[6], x[7]);
+    *reinterpret_cast<uint4*>(out + 8 * j) = o;
+    if (epi == HX_EPI_GELU) {
+      uint4 g;
+      g.x = pack_bf16(gelu_erf(x[0]), gelu_erf(x[1]));
+      g.y = pack_bf16(gelu_erf(x[2]), gelu_erf(x[3]));
+      g.z = pack_bf16(gelu_erf(x[4]), gelu_erf(x[5]));
+      g.w = pack_bf16(gelu_erf(x[6]), gelu_erf(x[7]));
+      *reinterpret_cast<uint4*>(out2 + 8 * j) = g;
+    }
+  }
+}
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    gemm_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
+                      const __grid_constant__ CUtensorMap tm_b, const GemmParams p) {
+  using C = GemmCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR_OFFSET);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const int num_m = (p.M + GEMM_BM - 1) / GEMM_BM;
+  const int num_n = (p.N + BN - 1) / BN;
+  const int num_tiles = num_m * num_n;
+  const int num_k = (p.K + GEMM_BK - 1) / GEMM_BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm_a);
+    tma_prefetch(&tm_b);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int mb, nb;
+        tile_coords(t, num_m, num_n, mb, nb);
+        const int m0 = mb * GEMM_BM, n0 = nb * BN;
+        for (int kb = 0; kb < num_k; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * C::STAGE_BYTES;
+          uint8_t* sb = sa + C::A_BYTES;
+          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          const int k0 = kb * GEMM_BK;
+          if (A_MN) {
+            tma_load_2d(sa, &tm_a, &full[stage], m0, k0);
+            tma_load_2d(sa + 8192, &tm_a, &full[stage], m0 + 64, k0);
+          } else {
+            tma_load_2d(sa, &tm_a, &full[stage], k0, m0);
+          }
+          if (B_MN) {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_2d(sb + j * 8192, &tm_b, &full[stage], n0 + 64 * j, k0);
+          } else {
+            tma_load_2d(sb, &tm_b, &full[stage], k0, n0);
+          }
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- UMMA issuer
+      constexpr uint32_t idesc = idesc_bf16(GEMM_BM, BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+        const int acc = it & 1;
+        mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_k; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
+          const uint32_t sb = sa + C::A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < GEMM_BK / 16; ++kk) {
+            const uint64_t da = A_MN ? sw128_desc(sa + kk * 2048, 8192, 1024)
+                                     : sw128_desc(sa + kk * 32, 16, 1024);
+            const uint64_t db = B_MN ? sw128_desc(sb + kk * 2048, 8192, 1024)
+                                     : sw128_desc(sb + kk * 32, 16, 1024);
+            umma_f16_ss(d_tmem, da, db, idesc, (kb | kk) != 0);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue
+    const int sub = warp & 3;  // TMEM lane quadrant this warp may access
+    int it = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      int mb, nb;
+      tile_coords(t, num_m, num_n, mb, nb);
+      const int acc = it & 1;
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const int row = mb * GEMM_BM + sub * 32 + lane;
+      const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(sub * 32) << 16);
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        const int col = nb * BN + c * 32;
+        if (col >= p.N) break;  // warp-uniform
+        uint32_t r[32];
+        tmem_ld32(taddr + c * 32, r);
+        tmem_wait_ld();
+        epilogue_chunk(p, row, col, r);
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, C::TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+
+template <int BN, bool A_MN, bool B_MN>
+static cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
+                               int num_sms, cudaStream_t stream) {
+  using C = GemmCfg<BN>;
+  auto kern = gemm_sm100_kernel<BN, A_MN, B_MN>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const int tiles = ((p.M + GEMM_BM - 1) / GEMM_BM) * ((p.N + BN - 1) / BN);
+  const int grid = tiles < num_sms ? tiles : num_sms;
+  kern<<<grid, GEMM_THREADS, C::SMEM_BYTES, stream>>>(ta, tb, p);
+  return cudaGetLastError();
+}
+
+static int pick_bn(int M, int N, int num_sms) {
+  if (N <= 128) return 128;
+  const long mb = (M + GEMM_BM - 1) / GEMM_BM;
+  const long t256 = mb * ((N + 255) / 256), t128 = mb * ((N + 127) / 128);
+  auto eff = [&](long tiles, double work_per_tile) {
+    const long waves = (tiles + num_sms - 1) / num_sms;
+    return (tiles * work_per_tile) / (waves * num_sms * work_per_tile);
+  };
+  // 256-wide tiles halve A re-reads and smem traffic per FLOP; only give them up
+  // for a clearly better wave quantisation.
+  return eff(t128, 1.0) > eff(t256, 1.0) + 0.12 ? 128 : 256;
+}
+
+cudaError_t gemm_launch(const GemmOperand& a, const GemmOperand& b, const GemmParams& p,
+                        cudaStream_t stream) {
+  int dev = 0, num_sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+  const int bn = pick_bn(p.M, p.N, num_sms);
+  CUtensorMap ta, tb;
+  // A: K-major [M,K] box {64,128}; MN-major [K,M] box {64,64}
+  cudaError_t e = a.mn ? make_tma_2d(&ta, a.ptr, p.K, p.M, a.ld, 64, 64)
+                       : make_tma_2d(&ta, a.ptr, p.M, p.K, a.ld, 64, GEMM_BM);
+  if (e != cudaSuccess) return e;
+  e = b.mn ? make_tma_2d(&tb, b.ptr, p.K, p.N, b.ld, 64, 64)
+           : make_tma_2d(&tb, b.ptr, p.N, p.K, b.ld, 64, bn);
+  if (e != cudaSuccess) return e;
+#define HX_GEMM_CASE(BN_, AM_, BM_)                                        \
+  if (bn == BN_ && a.mn == AM_ && b.mn == BM_)                               \
+    return launch_gemm<BN_, AM_, BM_>(ta, tb, p, num_sms, stream);
+  HX_GEMM_CASE(256, false, true)
+  HX_GEMM_CASE(256, false, false)
+  HX_GEMM_CASE(256, true, true)
+  HX_GEMM_CASE(128, false, true)
+  HX_GEMM_CASE(128, false, false)
+  HX_GEMM_CASE(128, true, true)
+#undef HX_GEMM_CASE
+  return cudaErrorNotSupported;
+}
+
+}  // namespace hx

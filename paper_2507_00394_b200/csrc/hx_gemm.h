@@ -1,0 +1,56 @@
+// Internal host/device interfaces shared by the libhx translation units.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/hx.h"
+
+namespace hx {
+
+struct GemmOperand {
+  const void* ptr;
+  int ld;    // row stride in elements of the stored matrix
+  bool mn;   // false: K contiguous; true: M (for A) / N (for B) contiguous
+};
+
+struct GemmParams {
+  int M, N, K;
+  int epi;               // HX_EPI_*
+  void* out;             // bf16 or f32 [M, N] with row stride ldo
+  int ldo;
+  const void* aux;       // bf16 [M, N]: residual (RESID) or GeLU pre-activation (DGELU)
+  int ld_aux;
+  void* out2;            // bf16 [M, N]: GeLU output (GELU)
+  int ldo2;
+};
+
+// 2-D bf16 tensor map over a row-major [rows, cols] matrix with row stride ld,
+// SWIZZLE_128B, box {box_cols, box_rows}.  OOB reads are zero-filled.
+cudaError_t make_tma_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint64_t ld,
+                        uint32_t box_cols, uint32_t box_rows);
+
+// 3-D bf16 tensor map over activations stored token-major [s][b][ld]: dims
+// {cols, b, s}, box {box_cols, 1, box_rows} (one batch column, box_rows tokens).
+cudaError_t make_tma_3d_rows(CUtensorMap* map, const void* ptr, uint64_t cols, uint64_t b, uint64_t s,
+                             uint64_t ld, uint32_t box_cols, uint32_t box_rows);
+
+cudaError_t ln_fwd_launch(const void* x, const float* g, const float* b, void* y, int rows, int h,
+                          cudaStream_t st);
+cudaError_t ln_bwd_launch(const void* dy, const void* x, const float* g, const void* dres, void* dx,
+                          float* dg, float* db, int rows, int h, cudaStream_t st);
+cudaError_t mse_loss_launch(const void* z, int64_t n, void* dz, double* sumsq, cudaStream_t st);
+cudaError_t axpy_f32_launch(float* y, const float* x, int64_t n, cudaStream_t st);
+cudaError_t attn_fwd_launch(const void* qkv, int ld_qkv, void* o, int ld_o, float* lse, int s, int b,
+                            int heads, int d, cudaStream_t st);
+cudaError_t attn_bwd_launch(const void* qkv, int ld_qkv, const void* o, const void* d_o, int ld_o,
+                            const float* lse, float* delta, float* dq_acc, void* dqkv, int ld_dqkv,
+                            int s, int b, int heads, int d, cudaStream_t st);
+
+cudaError_t gemm_launch(const GemmOperand& a, const GemmOperand& b, const GemmParams& p,
+                        cudaStream_t stream);
+
+int num_sms();
+
+}  // namespace hx

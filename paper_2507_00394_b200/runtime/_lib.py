@@ -1,0 +1,78 @@
+"""ctypes binding of libhx.so (the C-ABI declared in include/hx.h).
+
+There is no fallback: if the shared library is missing or a CUDA device is not
+available, every entry point raises :class:`KernelLibraryError`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent.parent
+LIB_PATH = Path(os.environ.get("HX_LIB", _PKG / "libhx.so"))
+
+HX_E = {1001: "HX_E_SHAPE", 1002: "HX_E_ALIGN", 1003: "HX_E_UNSUPPORTED"}
+
+EPI_STORE_BF16, EPI_RESID_BF16, EPI_GELU, EPI_DGELU, EPI_ACC_F32, EPI_STORE_F32 = range(6)
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_LL = ctypes.c_longlong
+
+# name -> argtypes (restype is int unless listed in _RESTYPE)
+SIGNATURES: dict[str, list] = {
+    "hx_version": [],
+    "hx_launch_count": [],
+    "hx_gemm": [_P, _I, _I, _P, _I, _I, _P, _I, _I, _I, _I, _I, _P, _I, _P, _I, _P],
+    "hx_ln_fwd": [_P, _P, _P, _P, _I, _I, _P],
+    "hx_ln_bwd": [_P, _P, _P, _P, _P, _P, _P, _I, _I, _P],
+    "hx_attn_fwd": [_P, _I, _P, _I, _P, _I, _I, _I, _I, _P],
+    "hx_attn_bwd": [_P, _I, _P, _P, _I, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P],
+    "hx_mse_loss": [_P, _LL, _P, _P, _P],
+    "hx_axpy_f32": [_P, _P, _LL, _P],
+    "hx_zero": [_P, _LL, _P],
+}
+_RESTYPE = {"hx_launch_count": ctypes.c_longlong}
+
+
+class KernelLibraryError(RuntimeError):
+    """libhx could not be loaded or a kernel call failed."""
+
+
+_lib = None
+
+
+def load(path: Path | str | None = None) -> ctypes.CDLL:
+    """Load (once) and type the library.  Loading needs no GPU."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise KernelLibraryError(
+            f"{p} not found: build it with `make` (or __graft_entry__.build()); "
+            "there is no CPU fallback for the stage-execution kernels")
+    lib = ctypes.CDLL(str(p))
+    for name, args in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = _RESTYPE.get(name, ctypes.c_int)
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        label = HX_E.get(rc, f"cudaError {rc}")
+        raise KernelLibraryError(f"{what} failed: {label}")
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args), name)
+
+
+def launch_count() -> int:
+    return int(load().hx_launch_count())

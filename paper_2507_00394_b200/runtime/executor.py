@@ -1,0 +1,739 @@
+"""Executes a helix / 1F1B / ZB1P schedule on B200s.
+
+Drop-in for ``pipelab.runtime.executor`` (``P/runtime/executor.py``):
+``execute_schedule(sched, params, inputs, mlp_chunk=None, threaded=False)``
+returns a :class:`RunResult` with the same fields, raising the same exception
+classes (``ExecutionError`` / ``PayloadMismatch`` / ``StalledSchedule``).
+
+Task semantics are the reference's (``executor.py:177-293``): FWD / BWD_B /
+BWD_W / RECOMPUTE_FWD run component math (here :class:`LayerMath`, i.e.
+libhx kernels); SEND moves the producer's payload after checking its element
+count against both the task volume and ``costs.comm_volume`` (hard error);
+RECV hands the payload to the consumer.  Gradients accumulate in fp32 device
+buffers; losses accumulate as sum(z^2) in fp64 device slots.
+
+Drivers
+  replay        one process, one CUDA stream, every stage time-multiplexed on
+                the current GPU, global dependency order exactly as the
+                reference's replay loop (``executor.py:297-332``).
+  multi-stream  ``threaded=True`` on one process: one CUDA stream per stage;
+                SEND records an event on the producer stream, the consumer
+                stream waits on it (the analogue of the reference's keyed
+                channels, ``executor.py:334-382``).
+  distributed   ``threaded=True`` under ``torch.distributed`` with world size
+                == n_stages: rank r runs stage r on its own GPU; every SEND /
+                RECV becomes a NCCL send / recv on a dedicated 2-rank
+                communicator per *directed* stage pair, receives posted in the
+                sender's issue order (no cross-direction FIFO deadlock, SURVEY
+                H5).  Pure ordering edges between stages (two-fold pair edges)
+                are not synchronised, as in the reference's threaded driver.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from ..costs import comm_volume
+from ..generators import meta_config
+from ..partition import post_stage, pre_stage
+from ..schedule import BWD_B, BWD_W, FWD, RECOMPUTE, RECV, SEND, Schedule, Task
+from .layers import LayerMath, payload_elements
+from .model import (MATRIX_FIELDS, PARAM_FIELDS, POST_FIELDS, PRE_FIELDS, DeviceLayer,
+                    LayerParams, layer_to_device)
+
+
+class ExecutionError(Exception):
+    pass
+
+
+class PayloadMismatch(ExecutionError):
+    """A transferred payload disagrees with the declared communication volume."""
+
+
+class StalledSchedule(ExecutionError):
+    """No stage can make progress (missing payload or unsatisfiable edge)."""
+
+
+@dataclass
+class RunResult:
+    losses: list[float]
+    param_grads: list[dict[str, np.ndarray]]
+    peak_stash_elements: list[int]
+    mode: str
+    timeline: dict[str, tuple[float, float]] | None = None   # device ms, if recorded
+
+
+# Stash entries that exist only for the flash backward (never part of the
+# reference's stash accounting, never sent between stages).
+_LOCAL_EXTRAS = ("o", "lse")
+
+
+def _logical_elements(entry: dict) -> int:
+    return sum(int(t.numel()) for k, t in entry.items() if k not in _LOCAL_EXTRAS)
+
+
+class _Stage:
+    def __init__(self, idx: int, device, stream):
+        self.idx = idx
+        self.device = device
+        self.stream = stream
+        self.values: dict[str, dict] = {}
+        self.stash: dict[tuple[int, int, str], dict] = {}
+        self.wctx: dict[int, list] = {}
+        self.peak = 0
+
+    def bump(self) -> None:
+        n = sum(_logical_elements(e) for e in self.stash.values())
+        for lst in self.wctx.values():
+            for _l, w_post, w_pre in lst:
+                n += _logical_elements(w_post) + _logical_elements(w_pre)
+        self.peak = max(self.peak, n)
+
+
+def stage_fields(sched: Schedule, stage: int, layer: int) -> tuple[tuple[str, ...], tuple[str, ...]]:
+    """(weights needed, gradient buffers owned) by ``stage`` for ``layer``."""
+    cfg = meta_config(sched)
+    chunked = any(t.comp == "chunk" for t in sched.tasks.values() if t.is_compute)
+    if chunked:
+        span = cfg.L // cfg.p
+        mine = layer // span == stage
+        return (PARAM_FIELDS, PARAM_FIELDS) if mine else ((), ())
+    need: tuple[str, ...] = ()
+    own: tuple[str, ...] = ()
+    if pre_stage(layer, cfg) == stage:
+        need += PRE_FIELDS
+        own += PRE_FIELDS
+    if post_stage(layer, cfg) == stage:
+        need += POST_FIELDS
+        own += POST_FIELDS
+    return need, own
+
+
+class DeviceModel:
+    """Per-layer device weights + fp32 gradient buffers for a set of local stages."""
+
+    def __init__(self, layers: dict[int, DeviceLayer]):
+        self.layers = layers
+
+    @staticmethod
+    def from_host(sched: Schedule, params: list[LayerParams], stages, device) -> "DeviceModel":
+        layers = {}
+        for l, p in enumerate(params):
+            need, own = set(), set()
+            for st in stages:
+                n, o = stage_fields(sched, st, l)
+                need.update(n)
+                own.update(o)
+            if need:
+                fields_ = tuple(f for f in PARAM_FIELDS if f in need)
+                layers[l] = DeviceLayer(layer_to_device(p, device, fields_),
+                                        tuple(f for f in PARAM_FIELDS if f in own))
+        return DeviceModel(layers)
+
+    def zero_grads(self, zero_fn) -> None:
+        for dl in self.layers.values():
+            dl.zero_grads(zero_fn)
+
+
+class _Core:
+    """Task interpreter shared by the drivers (``executor.py:136-293``)."""
+
+    def __init__(self, sched: Schedule, model: DeviceModel, math, stages: dict[int, _Stage],
+                 sumsq: torch.Tensor | None):
+        self.sched = sched
+        self.tasks = sched.tasks
+        self.cfg = meta_config(sched)
+        self.qkv = bool(int(sched.meta.get("qkv", 0)))
+        self.rc = bool(int(sched.meta.get("recompute", 0)))
+        self.split = sched.meta.get("backward") == "split"
+        self.model = model
+        self.math = math
+        self.stages = stages
+        self.sumsq = sumsq
+        self.inputs: list[torch.Tensor] = []
+        self.recv_of_send = {t.deps[0]: t.id for t in self.tasks.values() if t.kind == RECV}
+        self.sends_by_producer: dict[str, list[Task]] = {}
+        for t in self.tasks.values():
+            if t.kind == SEND:
+                self.sends_by_producer.setdefault(t.deps[0], []).append(t)
+        for lst in self.sends_by_producer.values():
+            lst.sort(key=lambda t: t.id)
+
+    # -- routing -------------------------------------------------------------------
+
+    def input_id(self, t: Task) -> str | None:
+        i, l = t.mb, t.layer
+        if t.kind == FWD:
+            if t.comp == "chunk":
+                c = f"rv.fb.s{t.stage}.m{i}"
+                return c if c in t.deps else None
+            if t.comp == "pre":
+                return f"f.post.l{l - 1}.m{i}" if l > 0 else None
+            tag, comp = {"attn": ("pa", "pre"), "post": ("ap", "attn")}[t.comp]
+            c = f"rv.{tag}.l{l}.m{i}"
+            return c if c in t.deps else f"f.{comp}.l{l}.m{i}"
+        if t.kind == BWD_B:
+            if t.comp == "chunk":
+                c = f"rv.gb.s{t.stage}.m{i}"
+                return c if c in t.deps else None
+            if t.comp == "post":
+                return f"b.pre.l{l + 1}.m{i}" if l < self.cfg.L - 1 else None
+            tag, comp = {"attn": ("gap", "post"), "pre": ("gpa", "attn")}[t.comp]
+            c = f"rv.{tag}.l{l}.m{i}"
+            return c if c in t.deps else f"b.{comp}.l{l}.m{i}"
+        return None
+
+    def take(self, st: _Stage, tid: str) -> dict:
+        try:
+            return st.values.pop(tid)
+        except KeyError:
+            raise StalledSchedule(f"stage {st.idx}: payload of {tid} not present") from None
+
+    def store_stash(self, st: _Stage, l: int, mb: int, comp: str, full: dict, payload: dict) -> None:
+        st.stash[(l, mb, comp)] = self.math.reduce_stash(comp, full, payload) if self.rc else full
+
+    def W(self, l: int):
+        return self.model.layers[l].w
+
+    def G(self, l: int):
+        return self.model.layers[l].grad
+
+    # -- compute tasks ------------------------------------------------------------------
+
+    def run_compute(self, t: Task) -> None:
+        st = self.stages[t.stage]
+        if t.kind == FWD:
+            (self._fwd_chunk if t.comp == "chunk" else self._fwd_component)(st, t)
+        elif t.kind == BWD_B:
+            (self._bwd_chunk if t.comp == "chunk" else self._bwd_component)(st, t)
+        elif t.kind == BWD_W:
+            for l, w_post, w_pre in st.wctx.pop(t.mb):
+                self.math.post_backward_w(w_post, self.G(l))
+                self.math.pre_backward_w(w_pre, self.G(l))
+        elif t.kind == RECOMPUTE:
+            key = (t.layer, t.mb, t.comp)
+            st.stash[key] = self.math.regenerate_stash(t.comp, st.stash[key],
+                                                       self.W(t.layer) if t.layer in self.model.layers else None)
+        else:
+            raise ExecutionError(f"{t.id}: kind {t.kind} is not a compute task")
+        st.bump()
+
+    def _loss(self, z: torch.Tensor, mb: int) -> torch.Tensor:
+        return self.math.loss(z, self.sumsq[mb:mb + 1])
+
+    def _fwd_component(self, st: _Stage, t: Task) -> None:
+        src = self.input_id(t)
+        if t.comp == "pre":
+            x = self.inputs[t.mb] if src is None else self.take(st, src)["x"]
+            payload, full = self.math.pre_forward(x, self.W(t.layer))
+            self.store_stash(st, t.layer, t.mb, "pre", full, {})
+            st.values[t.id] = payload
+        elif t.comp == "attn":
+            payload = self.take(st, src)
+            out, full = self.math.attn_forward(payload)
+            self.store_stash(st, t.layer, t.mb, "attn", full, payload)
+            st.values[t.id] = out
+        else:
+            payload = self.take(st, src)
+            out, full = self.math.post_forward(payload, self.W(t.layer))
+            self.store_stash(st, t.layer, t.mb, "post", full, payload)
+            st.values[t.id] = {"x": out}
+
+    def _bwd_component(self, st: _Stage, t: Task) -> None:
+        src = self.input_id(t)
+        l = t.layer
+        if t.comp == "post":
+            if src is None:
+                z = self.take(st, f"f.post.l{l}.m{t.mb}")["x"]
+                d_out = self._loss(z, t.mb)
+            else:
+                d_out = self.take(st, src)["d_x"]
+            stash = st.stash.pop((l, t.mb, "post"))
+            st.values[t.id] = self.math.post_backward(d_out, self.W(l), self.G(l), stash)
+        elif t.comp == "attn":
+            payload = self.take(st, src)
+            stash = st.stash.pop((l, t.mb, "attn"))
+            st.values[t.id] = self.math.attn_backward(payload, stash)
+        else:
+            payload = self.take(st, src)
+            stash = st.stash.pop((l, t.mb, "pre"))
+            d_x = self.math.pre_backward(payload, self.W(l), self.G(l), stash)
+            if l > 0:
+                st.values[t.id] = {"d_x": d_x}
+
+    def _fwd_chunk(self, st: _Stage, t: Task) -> None:
+        src = self.input_id(t)
+        x = self.inputs[t.mb] if src is None else self.take(st, src)["x"]
+        for l in range(t.layer, t.layer + t.span):
+            pa, s_pre = self.math.pre_forward(x, self.W(l))
+            self.store_stash(st, l, t.mb, "pre", s_pre, {})
+            ap, s_attn = self.math.attn_forward(pa)
+            self.store_stash(st, l, t.mb, "attn", s_attn, pa)
+            x, s_post = self.math.post_forward(ap, self.W(l))
+            self.store_stash(st, l, t.mb, "post", s_post, ap)
+        st.values[t.id] = {"x": x}
+
+    def _bwd_chunk(self, st: _Stage, t: Task) -> None:
+        src = self.input_id(t)
+        if src is None:
+            d = self._loss(self.take(st, f"f.s{t.stage}.m{t.mb}")["x"], t.mb)
+        else:
+            d = self.take(st, src)["d_x"]
+        deferred = []
+        for l in range(t.layer + t.span - 1, t.layer - 1, -1):
+            W, G = self.W(l), self.G(l)
+            gap, w_post = self.math.post_backward_b(d, W, G, st.stash.pop((l, t.mb, "post")))
+            gpa = self.math.attn_backward(gap, st.stash.pop((l, t.mb, "attn")))
+            d, w_pre = self.math.pre_backward_b(gpa, W, G, st.stash.pop((l, t.mb, "pre")))
+            if self.split:
+                deferred.append((l, w_post, w_pre))
+            else:
+                self.math.post_backward_w(w_post, G)
+                self.math.pre_backward_w(w_pre, G)
+        if self.split:
+            st.wctx[t.mb] = deferred
+        if t.stage > 0:
+            st.values[t.id] = {"d_x": d}
+
+    # -- comm ---------------------------------------------------------------------
+
+    def checked_payload(self, t: Task) -> dict:
+        payload = self.take(self.stages[t.stage], t.deps[0])
+        n = payload_elements(payload)
+        declared = comm_volume(self.cfg, t.edge, self.qkv)
+        if n != t.volume or n != declared:
+            raise PayloadMismatch(
+                f"{t.id}: payload carries {n} elements, task declares {t.volume}, "
+                f"cost model expects {declared} for edge {t.edge!r}")
+        return payload
+
+
+# ======================================================================================
+# drivers
+# ======================================================================================
+
+
+class _Timer:
+    """Per-task CUDA-event timeline on each stage's stream."""
+
+    def __init__(self, enabled: bool):
+        self.enabled = enabled
+        self.ev: dict[str, tuple[torch.cuda.Event, torch.cuda.Event]] = {}
+        self.t0: torch.cuda.Event | None = None
+
+    def start(self):
+        if self.enabled:
+            self.t0 = torch.cuda.Event(enable_timing=True)
+            self.t0.record()
+
+    def around(self, tid: str):
+        timer = self
+
+        class _Ctx:
+            def __enter__(self_):
+                if timer.enabled:
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record()
+                    timer.ev[tid] = (a, b)
+
+            def __exit__(self_, *exc):
+                if timer.enabled and exc[0] is None:
+                    timer.ev[tid][1].record()
+
+        return _Ctx()
+
+    def collect(self) -> dict[str, tuple[float, float]] | None:
+        if not self.enabled:
+            return None
+        torch.cuda.synchronize()
+        return {tid: (self.t0.elapsed_time(a), self.t0.elapsed_time(b)) for tid, (a, b) in self.ev.items()}
+
+
+def _replay(core: _Core, timer: _Timer) -> None:
+    """Single-threaded global-order driver (``executor.py:297-332``)."""
+    tasks, order = core.tasks, core.sched.per_stage_order
+    done: set[str] = set()
+    ptr = [0] * len(order)
+    comm = sorted(tid for tid, t in tasks.items() if not t.is_compute)
+    transit: dict[str, dict] = {}
+    while len(done) < len(tasks):
+        progressed = False
+        for tid in comm:
+            t = tasks[tid]
+            if tid in done or not all(d in done for d in t.deps):
+                continue
+            if t.kind == SEND:
+                transit[core.recv_of_send[tid]] = core.checked_payload(t)
+            else:
+                core.stages[t.stage].values[tid] = transit.pop(tid)
+            done.add(tid)
+            progressed = True
+        for si, seq in enumerate(order):
+            while ptr[si] < len(seq):
+                t = tasks[seq[ptr[si]]]
+                if not all(d in done for d in t.deps):
+                    break
+                with timer.around(t.id):
+                    core.run_compute(t)
+                done.add(t.id)
+                ptr[si] += 1
+                progressed = True
+        if not progressed:
+            blocked = {seq[ptr[si]]: [d for d in tasks[seq[ptr[si]]].deps if d not in done]
+                       for si, seq in enumerate(order) if ptr[si] < len(seq)}
+            raise StalledSchedule(f"schedule cannot progress; blocked on {blocked}")
+    if transit:
+        raise ExecutionError(f"undelivered payloads: {sorted(transit)}")
+
+
+def _multistream(core: _Core, timer: _Timer) -> None:
+    """One CUDA stream per stage on one GPU; host issues in replay order, the
+    device overlaps stages.  Cross-stage payloads are ordered by events."""
+    tasks, order = core.tasks, core.sched.per_stage_order
+    main = torch.cuda.current_stream()
+    streams = {si: torch.cuda.Stream() for si in core.stages}
+    start = torch.cuda.Event()
+    start.record(main)
+    for s in streams.values():
+        s.wait_event(start)
+    done: set[str] = set()
+    ptr = [0] * len(order)
+    events: dict[str, torch.cuda.Event] = {}
+    transit: dict[str, dict] = {}
+    comm = sorted(tid for tid, t in tasks.items() if not t.is_compute)
+    while len(done) < len(tasks):
+        progressed = False
+        for tid in comm:
+            t = tasks[tid]
+            if tid in done or not all(d in done for d in t.deps):
+                continue
+            if t.kind == SEND:
+                with torch.cuda.stream(streams[t.stage]):
+                    payload = core.checked_payload(t)
+                    ev = torch.cuda.Event()
+                    ev.record()
+                rid = core.recv_of_send[tid]
+                events[rid] = ev
+                transit[rid] = payload
+            else:
+                dst = streams[t.stage]
+                dst.wait_event(events.pop(tid))
+                payload = transit.pop(tid)
+                for tensor in payload.values():
+                    tensor.record_stream(dst)
+                core.stages[t.stage].values[tid] = payload
+            done.add(tid)
+            progressed = True
+        for si, seq in enumerate(order):
+            while ptr[si] < len(seq):
+                t = tasks[seq[ptr[si]]]
+                if not all(d in done for d in t.deps):
+                    break
+                with torch.cuda.stream(streams[si]), timer.around(t.id):
+                    core.run_compute(t)
+                done.add(t.id)
+                ptr[si] += 1
+                progressed = True
+        if not progressed:
+            raise StalledSchedule("schedule cannot progress (multi-stream)")
+    for s in streams.values():
+        end = torch.cuda.Event()
+        end.record(s)
+        main.wait_event(end)
+
+
+# --- distributed -----------------------------------------------------------------------
+
+
+def _payload_layout(cfg, edge_tag: str, qkv: bool) -> list[tuple[str, tuple, torch.dtype]]:
+    """Tensor names/shapes/dtypes of each edge's payload (``layers.py`` dict keys)."""
+    T, h = cfg.s * cfg.b, cfg.h
+    bf, f32 = torch.bfloat16, torch.float32
+    act = lambda n, w=h: (n, (T, w), bf)  # noqa: E731
+    if edge_tag == "pa":
+        return [act("ln_out"), act("residual"), ("qkv_weight", (h, 3 * h), bf)] if qkv \
+            else [act("qkv", 3 * h), act("residual")]
+    if edge_tag == "ap":
+        return [act("attn_out"), act("residual")]
+    if edge_tag == "gap":
+        return [act("d_attn_out"), act("d_residual")]
+    if edge_tag == "gpa":
+        return [act("d_ln_out"), act("d_residual"), ("d_qkv_weight", (h, 3 * h), f32)] if qkv \
+            else [act("d_qkv", 3 * h), act("d_residual")]
+    if edge_tag == "fb":
+        return [act("x")]
+    if edge_tag == "gb":
+        return [act("d_x")]
+    raise ExecutionError(f"unknown edge tag {edge_tag!r}")
+
+
+def _edge_tag(task_id: str) -> str:
+    return task_id.split(".")[1]
+
+
+class P2PPlan:
+    """Send / receive issue order per directed stage pair.
+
+    Rank r sends to q in the order its compute tasks run (per_stage_order[r],
+    then each producer's SENDs sorted by id, ``executor.py:127-132``).  The
+    receiver posts its RECVs from q in exactly that order, so FIFO matching on
+    the (q -> r) communicator pairs every message with the right buffer.
+    """
+
+    def __init__(self, sched: Schedule):
+        self.sched = sched
+        sends_by_producer: dict[str, list[Task]] = {}
+        recv_of_send = {}
+        for t in sched.tasks.values():
+            if t.kind == SEND:
+                sends_by_producer.setdefault(t.deps[0], []).append(t)
+            elif t.kind == RECV:
+                recv_of_send[t.deps[0]] = t.id
+        for lst in sends_by_producer.values():
+            lst.sort(key=lambda t: t.id)
+        n = sched.n_stages
+        self.send_seq: dict[tuple[int, int], list[str]] = {}
+        self.recv_seq: dict[tuple[int, int], list[str]] = {}
+        for src in range(n):
+            for tid in sched.per_stage_order[src]:
+                for snd in sends_by_producer.get(tid, ()):
+                    self.send_seq.setdefault((src, snd.peer), []).append(snd.id)
+                    self.recv_seq.setdefault((src, snd.peer), []).append(recv_of_send[snd.id])
+        self.pairs = sorted(self.send_seq)
+
+
+class _Distributed:
+    """Rank r executes stage r; payloads move over NCCL (or gloo on CPU tests)."""
+
+    def __init__(self, core: _Core, rank: int, groups: dict, lookahead: int = 1):
+        self.core = core
+        self.rank = rank
+        self.plan = P2PPlan(core.sched)
+        self.groups = groups
+        self.lookahead = lookahead
+        self.posted: dict[str, tuple[list, dict]] = {}    # rid -> (works, payload)
+        self.next_recv: dict[int, int] = {}               # src -> index into recv_seq
+        self.pending_sends: list = []
+
+    def _post_upto(self, src: int, rid: str) -> None:
+        seq = self.plan.recv_seq[(src, self.rank)]
+        want = seq.index(rid)
+        core, cfg = self.core, self.core.cfg
+        while self.next_recv.get(src, 0) <= min(want + self.lookahead, len(seq) - 1):
+            k = self.next_recv.get(src, 0)
+            r_id = seq[k]
+            layout = _payload_layout(cfg, _edge_tag(r_id), core.qkv)
+            st = core.stages[self.rank]
+            payload, works = {}, []
+            for name, shape, dtype in layout:
+                buf = torch.empty(shape, dtype=dtype, device=st.device)
+                payload[name] = buf
+                works.append(torch.distributed.irecv(buf, src=src, group=self.groups[(src, self.rank)]))
+            self.posted[r_id] = (works, payload)
+            self.next_recv[src] = k + 1
+
+    def _receive(self, rid: str) -> dict:
+        t = self.core.tasks[rid]
+        if rid not in self.posted:
+            self._post_upto(t.peer, rid)
+        works, payload = self.posted.pop(rid)
+        for w in works:
+            w.wait()
+        return payload
+
+    def run(self, timer: _Timer) -> None:
+        core, r = self.core, self.rank
+        st = core.stages[r]
+        for tid in core.sched.per_stage_order[r]:
+            t = core.tasks[tid]
+            for d in t.deps:
+                dt = core.tasks.get(d)
+                if dt is None or dt.kind != RECV or dt.stage != r or d in st.values:
+                    continue
+                st.values[d] = self._receive(d)
+            with timer.around(tid):
+                core.run_compute(t)
+            for snd in core.sends_by_producer.get(tid, ()):
+                payload = core.checked_payload(snd)
+                layout = _payload_layout(core.cfg, _edge_tag(snd.id), core.qkv)
+                grp = self.groups[(r, snd.peer)]
+                for name, _shape, dtype in layout:
+                    tensor = payload[name].contiguous()
+                    if tensor.dtype != dtype:
+                        raise PayloadMismatch(f"{snd.id}: {name} has dtype {tensor.dtype}, want {dtype}")
+                    self.pending_sends.append((torch.distributed.isend(tensor, dst=snd.peer, group=grp), tensor))
+        for w, _t in self.pending_sends:
+            w.wait()
+        self.pending_sends.clear()
+        if self.posted:
+            raise ExecutionError(f"undelivered payloads: {sorted(self.posted)}")
+
+
+def make_pair_groups(n_stages: int) -> dict[tuple[int, int], object]:
+    """One 2-rank group per directed stage pair; every rank must call this in
+    the same order (``torch.distributed.new_group`` is collective)."""
+    groups = {}
+    for a in range(n_stages):
+        for b in range(n_stages):
+            if a != b:
+                groups[(a, b)] = torch.distributed.new_group([a, b])
+    return groups
+
+
+# ======================================================================================
+# public API
+# ======================================================================================
+
+
+class HelixRuntime:
+    """Device-resident state for repeatedly executing one schedule.
+
+    ``run(inputs)`` enqueues one full iteration (all micro-batches, forward and
+    backward, gradient accumulation) without synchronising the host; the
+    benchmark times it with CUDA events.  ``result()`` synchronises and
+    returns a :class:`RunResult`.
+    """
+
+    def __init__(self, sched: Schedule, model: DeviceModel, mlp_chunk: int | None = None,
+                 mode: str = "replay", device=None, math=None, rank: int | None = None,
+                 groups: dict | None = None, record_timeline: bool = False):
+        self.sched = sched
+        self.cfg = meta_config(sched)
+        self.mode = mode
+        self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        qkv = bool(int(sched.meta.get("qkv", 0)))
+        self.math = math if math is not None else LayerMath(self.cfg, qkv, mlp_chunk, self.device)
+        self.model = model
+        self.rank = rank
+        local = [rank] if mode == "distributed" else list(range(sched.n_stages))
+        self.stages = {si: _Stage(si, self.device, None) for si in local}
+        self.sumsq = torch.zeros(self.cfg.m, dtype=torch.float64, device=self.device)
+        self.core = _Core(sched, model, self.math, self.stages, self.sumsq)
+        self.groups = groups
+        self.record_timeline = record_timeline
+        self.timeline = None
+
+    def run(self, inputs: list[torch.Tensor]) -> None:
+        cfg = self.cfg
+        if len(inputs) != cfg.m:
+            raise ExecutionError(f"need {cfg.m} input microbatches, got {len(inputs)}")
+        self.core.inputs = [x.reshape(cfg.s * cfg.b, cfg.h) for x in inputs]
+        for st in self.stages.values():
+            st.peak = 0
+        self.model.zero_grads(self.math.zero_)
+        self.math.zero_(self.sumsq)
+        timer = _Timer(self.record_timeline)
+        timer.start()
+        if self.mode == "replay":
+            _replay(self.core, timer)
+        elif self.mode == "multistream":
+            _multistream(self.core, timer)
+        elif self.mode == "distributed":
+            _Distributed(self.core, self.rank, self.groups).run(timer)
+        else:
+            raise ExecutionError(f"unknown mode {self.mode!r}")
+        self.timeline = timer.collect()
+        self._check_drained()
+
+    def _check_drained(self) -> None:
+        leftovers = sorted(tid for st in self.stages.values() for tid in st.values)
+        if leftovers:
+            raise ExecutionError(f"unconsumed payloads: {leftovers[:6]}")
+        dirty = [st.idx for st in self.stages.values() if st.stash or st.wctx]
+        if dirty:
+            raise ExecutionError(f"stash not drained on stages {dirty}")
+
+    def loss_stage(self, mb: int) -> int:
+        chunked = any(t.comp == "chunk" for t in self.sched.tasks.values() if t.is_compute)
+        return 0 if chunked else post_stage(self.cfg.L - 1, self.cfg)
+
+    def losses(self) -> list[float]:
+        n = self.cfg.s * self.cfg.b * self.cfg.h
+        return [float(v) / n for v in self.sumsq.cpu().tolist()]
+
+    def grads_numpy(self) -> dict[int, dict[str, np.ndarray]]:
+        return {l: {k: g.double().cpu().numpy() for k, g in dl.grad.items()}
+                for l, dl in self.model.layers.items()}
+
+
+def _to_device_inputs(inputs, cfg, device) -> list[torch.Tensor]:
+    out = []
+    for i, x in enumerate(inputs):
+        shape = tuple(x.shape)
+        if shape != (cfg.s, cfg.b, cfg.h):
+            raise ExecutionError(f"input {i} has shape {shape}, want {(cfg.s, cfg.b, cfg.h)}")
+        t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))
+        out.append(t.to(device=device, dtype=torch.bfloat16).reshape(cfg.s * cfg.b, cfg.h).contiguous())
+    return out
+
+
+def execute_schedule(sched: Schedule, params: list[LayerParams], inputs: list,
+                     mlp_chunk: int | None = None, threaded: bool = False,
+                     record_timeline: bool = False) -> RunResult:
+    """Run ``sched`` numerically on the B200(s); same contract as the reference.
+
+    ``threaded=False``: replay on the current GPU.  ``threaded=True``: one rank
+    per stage when ``torch.distributed`` is initialised with world size ==
+    n_stages (every rank calls this and gets the same, all-gathered result),
+    otherwise one CUDA stream per stage on the current GPU.
+    """
+    cfg = meta_config(sched)
+    if len(params) != cfg.L:
+        raise ExecutionError(f"need {cfg.L} layer params, got {len(params)}")
+    if len(inputs) != cfg.m:
+        raise ExecutionError(f"need {cfg.m} input microbatches, got {len(inputs)}")
+    if not torch.cuda.is_available():
+        raise ExecutionError("execute_schedule needs a CUDA device (no CPU fallback)")
+    device = torch.device("cuda", torch.cuda.current_device())
+    dist = threaded and torch.distributed.is_available() and torch.distributed.is_initialized() \
+        and torch.distributed.get_world_size() == sched.n_stages
+    if dist:
+        rank = torch.distributed.get_rank()
+        model = DeviceModel.from_host(sched, params, [rank], device)
+        rt = HelixRuntime(sched, model, mlp_chunk, "distributed", device, rank=rank,
+                          groups=make_pair_groups(sched.n_stages), record_timeline=record_timeline)
+    else:
+        model = DeviceModel.from_host(sched, params, range(sched.n_stages), device)
+        rt = HelixRuntime(sched, model, mlp_chunk, "multistream" if threaded else "replay", device,
+                          record_timeline=record_timeline)
+    rt.run(_to_device_inputs(inputs, cfg, device))
+    torch.cuda.synchronize()
+    if dist:
+        return _gather_distributed(rt, params)
+    grads = rt.grads_numpy()
+    losses = rt.losses()
+    peaks = [rt.stages[i].peak for i in range(sched.n_stages)]
+    return RunResult(losses, [grads[l] for l in range(cfg.L)], peaks, "threaded" if threaded else "replay",
+                     rt.timeline)
+
+
+def _gather_distributed(rt: HelixRuntime, params) -> RunResult:
+    """All ranks contribute their owned gradients, loss slots and peaks."""
+    import torch.distributed as dist
+    local = {"grads": rt.grads_numpy(), "sumsq": rt.sumsq.cpu().tolist(),
+             "peak": rt.stages[rt.rank].peak, "rank": rt.rank, "timeline": rt.timeline}
+    allv = [None] * dist.get_world_size()
+    dist.all_gather_object(allv, local)
+    cfg = rt.cfg
+    n = cfg.s * cfg.b * cfg.h
+    sumsq = np.zeros(cfg.m)
+    grads: list[dict[str, np.ndarray]] = [{} for _ in range(cfg.L)]
+    for part in allv:
+        sumsq += np.array(part["sumsq"])
+        for l, g in part["grads"].items():
+            for k, v in g.items():
+                if k in grads[l]:
+                    raise ExecutionError(f"gradient site ({l}, {k}) recorded on two stages")
+                grads[l][k] = v
+    for l in range(cfg.L):
+        missing = [k for k in PARAM_FIELDS if k not in grads[l]]
+        if missing:
+            raise ExecutionError(f"gradient sites missing: {[(l, k) for k in missing][:6]}")
+    peaks = [p["peak"] for p in sorted(allv, key=lambda p: p["rank"])]
+    tl = {}
+    for part in allv:
+        tl.update(part["timeline"] or {})
+    return RunResult(list(sumsq / n), grads, peaks, "threaded", tl or None)

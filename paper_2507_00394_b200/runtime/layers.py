@@ -1,0 +1,209 @@
+"""Transformer-layer components on the B200: pre / attention / post, forward and
+fused backward, recompute-stash management.
+
+Mirrors ``P/runtime/layers.py`` component by component (same payload and stash
+dictionary keys, so the executor's payload-size contract with
+``costs.comm_volume`` holds unchanged), but every op is a libhx kernel:
+
+  pre   fwd  LN1                                   hx_ln_fwd
+  attn  fwd  QKV GEMM, flash attention             hx_gemm, hx_attn_fwd
+  post  fwd  O GEMM + residual, LN2, W1 GEMM + GeLU, W2 GEMM + residual
+  post  bwd  W2^T GEMM * GeLU', W1^T GEMM, LN2 bwd + residual, Wo^T GEMM,
+             three weight-gradient GEMMs accumulating into fp32
+  attn  bwd  (recompute QKV), flash backward, Wqkv^T GEMM, dWqkv GEMM
+  pre   bwd  LN1 bwd + residual, dWqkv accumulate
+
+Layout: activations are bf16 ``[s*b, width]`` (token-major).  Besides the
+reference's stash entries the attention stash keeps the attention output O and
+its row LSE (flash backward needs them instead of the full probability
+matrix); both are attention-stage-local and never cross a stage boundary.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import kernels as K
+
+BF16 = torch.bfloat16
+Arrays = dict[str, torch.Tensor]
+
+
+def payload_elements(payload: Arrays) -> int:
+    return sum(int(t.numel()) for t in payload.values())
+
+
+class LayerMath:
+    """Component kernels for one model shape; owns the attention workspaces."""
+
+    def __init__(self, cfg, qkv_in_attention: bool, mlp_chunk: int | None, device):
+        self.cfg = cfg
+        self.qkv = qkv_in_attention
+        self.chunk = mlp_chunk
+        self.device = device
+        self.T = cfg.s * cfg.b
+        self.h = cfg.h
+        self.heads = cfg.num_heads
+
+    def zero_(self, t: torch.Tensor) -> torch.Tensor:
+        return K.zero_(t)
+
+    # -- helpers ------------------------------------------------------------------
+
+    def _empty(self, width: int, dtype=BF16) -> torch.Tensor:
+        return torch.empty(self.T, width, dtype=dtype, device=self.device)
+
+    def _row_slabs(self):
+        """Row ranges of the chunked MLP (``mathops.py:132-142``): chunks of c
+        sequence positions = c*b token rows; None means one slab."""
+        s, b = self.cfg.s, self.cfg.b
+        c = s if self.chunk is None else min(self.chunk, s)
+        return [(a * b, min(a + c, s) * b) for a in range(0, s, c)]
+
+    # -- forward ----------------------------------------------------------------------
+
+    def pre_forward(self, x: torch.Tensor, W) -> tuple[Arrays, Arrays]:
+        ln_out = K.layernorm(x, W["ln1_gain"], W["ln1_bias"], self._empty(self.h))
+        if self.qkv:
+            return {"ln_out": ln_out, "residual": x, "qkv_weight": W["qkv_weight"]}, {"x": x}
+        qkv = K.linear(ln_out, W["qkv_weight"], self._empty(3 * self.h))
+        return {"qkv": qkv, "residual": x}, {"x": x, "ln_out": ln_out}
+
+    def _attention(self, qkv: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+        o = self._empty(self.h)
+        lse = torch.empty(self.cfg.b, self.heads, self.cfg.s, dtype=torch.float32, device=self.device)
+        K.attention_fwd(qkv, self.cfg.s, self.cfg.b, self.heads, o, lse)
+        return o, lse
+
+    def attn_forward(self, payload: Arrays) -> tuple[Arrays, Arrays]:
+        if self.qkv:
+            qkv = K.linear(payload["ln_out"], payload["qkv_weight"], self._empty(3 * self.h))
+            stash = {"ln_out": payload["ln_out"], "qkv": qkv, "qkv_weight": payload["qkv_weight"]}
+        else:
+            qkv = payload["qkv"]
+            stash = {"qkv": qkv}
+        o, lse = self._attention(qkv)
+        stash["o"], stash["lse"] = o, lse
+        return {"attn_out": o, "residual": payload["residual"]}, stash
+
+    def _post_trunk(self, attn_out, residual, W) -> Arrays:
+        x2 = K.linear_resid(attn_out, W["o_weight"], residual, self._empty(self.h))
+        ln2 = K.layernorm(x2, W["ln2_gain"], W["ln2_bias"], self._empty(self.h))
+        m1 = self._empty(4 * self.h)
+        g = self._empty(4 * self.h)
+        for a, e in self._row_slabs():
+            K.linear_gelu(ln2[a:e], W["mlp_w1"], m1[a:e], g[a:e])
+        return {"attn_out": attn_out, "x2": x2, "ln2_out": ln2, "m1": m1, "g": g}
+
+    def post_forward(self, payload: Arrays, W) -> tuple[torch.Tensor, Arrays]:
+        t = self._post_trunk(payload["attn_out"], payload["residual"], W)
+        out = self._empty(self.h)
+        for a, e in self._row_slabs():
+            K.linear_resid(t["g"][a:e], W["mlp_w2"], t["x2"][a:e], out[a:e])
+        return out, t
+
+    # -- loss ---------------------------------------------------------------------------
+
+    def loss(self, z: torch.Tensor, sumsq_slot: torch.Tensor) -> torch.Tensor:
+        dz = torch.empty_like(z)
+        K.mse_loss(z, dz, sumsq_slot)
+        return dz
+
+    # -- backward (fused B + W) ------------------------------------------------------------
+
+    def post_backward_b(self, d_out: torch.Tensor, W, G, stash: Arrays) -> tuple[Arrays, Arrays]:
+        """Input-gradient half (``layers.py:143-154``).  The LN2 gain/bias
+        gradients are row reductions the LN-backward kernel produces anyway, so
+        they accumulate here; the three weight GEMMs go to the W half."""
+        d_m1 = self._empty(4 * self.h)
+        d_ln2 = self._empty(self.h)
+        for a, e in self._row_slabs():
+            K.linear_dx_dgelu(d_out[a:e], W["mlp_w2"], stash["m1"][a:e], d_m1[a:e])
+            K.linear_dx(d_m1[a:e], W["mlp_w1"], d_ln2[a:e])
+        d_x2 = self._empty(self.h)
+        K.layernorm_bwd(d_ln2, stash["x2"], W["ln2_gain"], d_out, d_x2,
+                        G["ln2_gain"], G["ln2_bias"])
+        d_attn = K.linear_dx(d_x2, W["o_weight"], self._empty(self.h))
+        wctx = {"attn_out": stash["attn_out"], "d_o": d_x2, "ln2_out": stash["ln2_out"],
+                "d_m1": d_m1, "g": stash["g"], "d_out": d_out}
+        return {"d_attn_out": d_attn, "d_residual": d_x2}, wctx
+
+    def post_backward_w(self, wctx: Arrays, G) -> None:
+        """Weight-gradient half (``layers.py:157-162``): fp32 accumulate over all rows."""
+        K.linear_dw(wctx["attn_out"], wctx["d_o"], G["o_weight"])
+        K.linear_dw(wctx["ln2_out"], wctx["d_m1"], G["mlp_w1"])
+        K.linear_dw(wctx["g"], wctx["d_out"], G["mlp_w2"])
+
+    def post_backward(self, d_out: torch.Tensor, W, G, stash: Arrays) -> Arrays:
+        """Fused backward of the post component (B then W immediately)."""
+        gap, wctx = self.post_backward_b(d_out, W, G, stash)
+        self.post_backward_w(wctx, G)
+        return gap
+
+    def attn_backward(self, payload: Arrays, stash: Arrays) -> Arrays:
+        """``layers.attn_backward`` (``layers.py:165-184``)."""
+        qkv = stash.get("qkv")
+        if qkv is None:  # recompute retention: rebuild the projection, never the attention
+            qkv = K.linear(stash["ln_out"], stash["qkv_weight"], self._empty(3 * self.h))
+        d_qkv = self._empty(3 * self.h)
+        # workspaces come from the stream-ordered caching allocator so that
+        # stages on different streams never share them
+        delta = torch.empty(self.cfg.b * self.heads * self.cfg.s, dtype=torch.float32, device=self.device)
+        dq = torch.empty(self.T * self.h, dtype=torch.float32, device=self.device)
+        K.attention_bwd(qkv, stash["o"], payload["d_attn_out"], stash["lse"], self.cfg.s,
+                        self.cfg.b, self.heads, d_qkv, delta, dq)
+        if not self.qkv:
+            return {"d_qkv": d_qkv, "d_residual": payload["d_residual"]}
+        d_ln = K.linear_dx(d_qkv, stash["qkv_weight"], self._empty(self.h))
+        d_w = torch.empty(self.h, 3 * self.h, dtype=torch.float32, device=self.device)
+        K.linear_dw(stash["ln_out"], d_qkv, d_w, accumulate=False)
+        return {"d_ln_out": d_ln, "d_residual": payload["d_residual"], "d_qkv_weight": d_w}
+
+    def pre_backward_b(self, payload: Arrays, W, G, stash: Arrays) -> tuple[torch.Tensor, Arrays]:
+        """Input-gradient half (``layers.py:187-198``) + LN1 gain/bias grads."""
+        if self.qkv:
+            d_ln = payload["d_ln_out"]
+            wctx = {"d_qkv_weight": payload["d_qkv_weight"]}
+        else:
+            d_ln = K.linear_dx(payload["d_qkv"], W["qkv_weight"], self._empty(self.h))
+            wctx = {"ln_out": stash["ln_out"], "d_qkv": payload["d_qkv"]}
+        d_x = self._empty(self.h)
+        K.layernorm_bwd(d_ln, stash["x"], W["ln1_gain"], payload["d_residual"], d_x,
+                        G["ln1_gain"], G["ln1_bias"])
+        return d_x, wctx
+
+    def pre_backward_w(self, wctx: Arrays, G) -> None:
+        """Weight-gradient half (``layers.py:201-207``)."""
+        if "d_qkv_weight" in wctx:
+            K.axpy(G["qkv_weight"], wctx["d_qkv_weight"])
+        else:
+            K.linear_dw(wctx["ln_out"], wctx["d_qkv"], G["qkv_weight"])
+
+    def pre_backward(self, payload: Arrays, W, G, stash: Arrays) -> torch.Tensor:
+        d_x, wctx = self.pre_backward_b(payload, W, G, stash)
+        self.pre_backward_w(wctx, G)
+        return d_x
+
+    # -- recompute (layers.py:213-247) -------------------------------------------------------
+
+    def reduce_stash(self, comp: str, stash: Arrays, payload: Arrays) -> Arrays:
+        if comp == "pre":
+            return {"x": stash["x"]}
+        if comp == "attn":
+            keep = {"ln_out": stash["ln_out"], "qkv_weight": stash["qkv_weight"]} if self.qkv \
+                else {"qkv": stash["qkv"]}
+            keep["o"], keep["lse"] = stash["o"], stash["lse"]
+            return keep
+        if comp == "post":
+            return {"attn_out": payload["attn_out"], "residual": payload["residual"]}
+        raise ValueError(f"no recompute retention for component {comp!r}")
+
+    def regenerate_stash(self, comp: str, kept: Arrays, W) -> Arrays:
+        if comp == "pre":
+            if self.qkv:
+                return {"x": kept["x"]}
+            return {"x": kept["x"],
+                    "ln_out": K.layernorm(kept["x"], W["ln1_gain"], W["ln1_bias"], self._empty(self.h))}
+        if comp == "post":
+            return self._post_trunk(kept["attn_out"], kept["residual"], W)
+        raise ValueError(f"component {comp!r} is never recomputed")

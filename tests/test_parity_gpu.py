@@ -1,0 +1,126 @@
+"""End-to-end parity on the B200: ``execute_schedule`` (libhx kernels, bf16 with
+fp32 accumulation) against the float64 oracle on the same seeded inputs.
+
+Stated tolerances (bf16 activations / weights, fp32 accumulation and grads):
+  loss            |got - ref| / ref                     <= 2e-3
+  each gradient   cosine(got, ref)                      >= 0.9995
+                  max|got - ref| / max|ref|             <= 2e-2
+The schedule itself is bit-exact (tests/test_schedule_parity.py).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle import helix_oracle as O  # noqa: E402
+from paper_2507_00394_b200 import METHODS, ModelConfig, generate  # noqa: E402
+from paper_2507_00394_b200.costs import DurationTable  # noqa: E402
+from paper_2507_00394_b200.runtime import (PayloadMismatch, StalledSchedule,  # noqa: E402
+                                           execute_schedule, make_inputs, make_model)
+
+UNIT = DurationTable.from_units(1, 3, 2)
+LOSS_TOL, COS_TOL, MAX_TOL = 2e-3, 0.9995, 2e-2
+
+SMALL = ModelConfig(L=2, h=128, s=256, b=1, num_heads=2, p=2, m=4)      # head_dim 64
+WIDE = ModelConfig(L=2, h=256, s=384, b=2, num_heads=2, p=2, m=4)       # head_dim 128, b=2
+TINY = ModelConfig(L=4, h=256, s=1024, b=1, num_heads=4, p=2, m=4)      # BASELINE config 1
+TINY_LOSSES = [3.327261203817688, 3.3800507339316543, 3.443091222231624, 3.4279542847160513]
+
+_ORACLE_CACHE = {}
+
+
+def oracle_for(cfg, pseed=0, iseed=1, chunk=None):
+    key = (cfg, pseed, iseed)
+    if key not in _ORACLE_CACHE:
+        params = O.make_model(cfg.L, cfg.h, pseed)
+        inputs = O.make_inputs(cfg.m, cfg.s, cfg.b, cfg.h, iseed)
+        _ORACLE_CACHE[key] = O.sequential_oracle(params, inputs, cfg.num_heads, chunk)
+    return _ORACLE_CACHE[key]
+
+
+def compare(res, ref, L, label=""):
+    worst = {"loss": 0.0, "cos": 1.0, "max": 0.0}
+    for got, want in zip(res.losses, ref.losses):
+        worst["loss"] = max(worst["loss"], abs(got - want) / abs(want))
+    for l in range(L):
+        for k in O.FIELDS:
+            g, r = res.param_grads[l][k].ravel(), ref.param_grads[l][k].ravel()
+            cos = float(g @ r / (np.linalg.norm(g) * np.linalg.norm(r)))
+            mx = float(np.abs(g - r).max() / np.abs(r).max())
+            worst["cos"] = min(worst["cos"], cos)
+            worst["max"] = max(worst["max"], mx)
+    print(f"[parity] {label} worst loss rel {worst['loss']:.2e} cos {worst['cos']:.6f} max {worst['max']:.2e}")
+    assert worst["loss"] <= LOSS_TOL, worst
+    assert worst["cos"] >= COS_TOL, worst
+    assert worst["max"] <= MAX_TOL, worst
+    return worst
+
+
+def run(cfg, method, pseed=0, iseed=1, **kw):
+    sched = generate(method, cfg, UNIT)
+    return execute_schedule(sched, make_model(cfg, pseed), make_inputs(cfg, iseed), **kw)
+
+
+@pytest.mark.parametrize("method", METHODS)
+def test_every_method_matches_oracle_small(method):
+    res = run(SMALL, method)
+    assert res.mode == "replay"
+    compare(res, oracle_for(SMALL), SMALL.L, f"small {method}")
+
+
+@pytest.mark.parametrize("method", ["helix_twofold", "helix_twofold_rc", "1f1b"])
+def test_head_dim_128_batch_2_matches_oracle(method):
+    compare(run(WIDE, method), oracle_for(WIDE), WIDE.L, f"wide {method}")
+
+
+def test_multistream_equals_replay_within_tolerance():
+    a = run(SMALL, "helix_twofold")
+    b = run(SMALL, "helix_twofold", threaded=True)
+    assert b.mode == "threaded"
+    compare(b, oracle_for(SMALL), SMALL.L, "small multistream")
+    assert np.allclose(a.losses, b.losses, rtol=1e-3)
+
+
+def test_chunk_and_recompute_invariance():
+    ref = oracle_for(SMALL)
+    for chunk in (64, 100, None):
+        compare(run(SMALL, "helix_twofold_rc", mlp_chunk=chunk), ref, SMALL.L, f"rc chunk={chunk}")
+
+
+def test_tiny_baseline_config_against_oracle():
+    res = run(TINY, "helix_twofold")
+    for got, want in zip(res.losses, TINY_LOSSES):
+        assert abs(got - want) / want <= LOSS_TOL
+    compare(res, oracle_for(TINY), TINY.L, "tiny helix_twofold")
+
+
+def test_peak_stash_accounting_matches_reference_formula():
+    cfg = SMALL
+    bsh = cfg.b * cfg.s * cfg.h
+    res = run(cfg, "helix_twofold")
+    full = (16 * bsh + 3 * cfg.h * cfg.h) * cfg.m * cfg.L // cfg.p
+    assert res.peak_stash_elements == [full] * cfg.p
+    rc = run(cfg, "helix_twofold_rc")
+    kept = (4 * bsh + 3 * cfg.h * cfg.h) * cfg.m * cfg.L // cfg.p
+    assert all(kept <= pk <= kept + 16 * bsh for pk in rc.peak_stash_elements)
+
+
+def test_rejects_wrong_volume():
+    from dataclasses import replace
+    sched = generate("helix_naive", SMALL, UNIT)
+    sid = next(t.id for t in sched.tasks.values() if t.kind == "SEND")
+    sched.tasks[sid] = replace(sched.tasks[sid], volume=sched.tasks[sid].volume + 1)
+    with pytest.raises(PayloadMismatch):
+        execute_schedule(sched, make_model(SMALL, 0), make_inputs(SMALL, 1))
+
+
+def test_reports_stall():
+    sched = generate("1f1b", SMALL, UNIT)
+    sched.per_stage_order[0].reverse()
+    with pytest.raises(StalledSchedule):
+        execute_schedule(sched, make_model(SMALL, 0), make_inputs(SMALL, 1))

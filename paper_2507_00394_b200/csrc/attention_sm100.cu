@@ -265,6 +265,232 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 }
 
 // =====================================================================================
+// forward v2: two query tiles per CTA, ping-pong softmax, P in TMEM
+// =====================================================================================
+//
+// CTA = query tiles (2t, 2t+1) of one (batch, head).  Two softmax warpgroups
+// (warps 0-3 -> tile A, 4-7 -> tile B) alternate with the tensor core: while
+// group A exponentiates S_A(j), the tensor core runs O_B += P_B(j-1) V(j-1) and
+// S_B(j) = Q_B K(j)^T, and vice versa.  P is written back as bf16 into the
+// first 64 columns of its own S region and consumed from TMEM by the
+// PV tcgen05.mma (A operand in TMEM), so P never touches shared memory.
+// O is rescaled only when a row's running max grows by more than 2^8
+// (exponents stay <= 256, exact in fp32), which makes rescales rare.
+//
+// TMEM (512 columns): S_A 0-127 | S_B 128-255 | O_A 256-383 | O_B 384-511.
+
+constexpr int FWD2_THREADS = 320;  // 8 softmax warps + TMA warp + MMA warp
+
+template <int D>
+struct Fwd2Smem {
+  static constexpr int QA = 0;
+  static constexpr int QB = QA + Tile<D>::BYTES;
+  static constexpr int KV = QB + Tile<D>::BYTES;  // 2 stages x (K, V)
+  static constexpr int BAR = KV + 4 * Tile<D>::BYTES;
+  static constexpr int TOTAL = BAR + 256 + 1024;
+};
+
+HX_DEVICE float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+template <int D>
+__global__ void __launch_bounds__(FWD2_THREADS, 1)
+    attn_fwd2_kernel(const __grid_constant__ CUtensorMap tm_qkv, const AttnParams p) {
+  using L = Fwd2Smem<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR);
+  uint64_t* q_full = bars;          // 1
+  uint64_t* k_full = bars + 1;      // 2
+  uint64_t* v_full = bars + 3;      // 2
+  uint64_t* kv_empty = bars + 5;    // 2
+  uint64_t* s_full = bars + 7;      // 2 (per group)
+  uint64_t* p_full = bars + 9;      // 2
+  uint64_t* o_full = bars + 11;     // 2
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
+
+  const int warp = warp_id(), lane = lane_id();
+  const int nq = (p.s + AT_TILE - 1) / AT_TILE;
+  const int npairs = (nq + 1) / 2;
+  const int t = npairs - 1 - static_cast<int>(blockIdx.x);  // heaviest pairs first
+  const int qtile[2] = {2 * t, 2 * t + 1};
+  const bool has_b = qtile[1] < nq;
+  const int last[2] = {qtile[0], has_b ? qtile[1] : -1};
+  const int nkv = has_b ? qtile[1] + 1 : qtile[0] + 1;
+  const int bh = blockIdx.y;
+  const int bi = bh / p.heads, head = bh % p.heads;
+  const int qcol = head * D, kcol = p.h + head * D, vcol = 2 * p.h + head * D;
+
+  if (warp == 8 && lane == 0) {
+    tma_prefetch(&tm_qkv);
+    for (int i = 0; i < 13; ++i) mbar_init(&bars[i], (i == 9 || i == 10) ? 128 : 1);
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 8) {
+    if (lane == 0) {  // ---------------- TMA producer
+      mbar_arrive_expect_tx(q_full, (has_b ? 2 : 1) * Tile<D>::BYTES);
+      tma_tile<D>(smem + L::QA, &tm_qkv, q_full, qcol, bi, qtile[0] * AT_TILE);
+      if (has_b) tma_tile<D>(smem + L::QB, &tm_qkv, q_full, qcol, bi, qtile[1] * AT_TILE);
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j & 1;
+        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        uint8_t* kb = smem + L::KV + st * 2 * Tile<D>::BYTES;
+        mbar_arrive_expect_tx(&k_full[st], Tile<D>::BYTES);
+        tma_tile<D>(kb, &tm_qkv, &k_full[st], kcol, bi, j * AT_TILE);
+        mbar_arrive_expect_tx(&v_full[st], Tile<D>::BYTES);
+        tma_tile<D>(kb + Tile<D>::BYTES, &tm_qkv, &v_full[st], vcol, bi, j * AT_TILE);
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      constexpr uint32_t id_s = idesc_bf16(128, 128, false, false);
+      constexpr uint32_t id_o = idesc_bf16(128, D, false, true);
+      const uint32_t sq[2] = {smem_u32(smem + L::QA), smem_u32(smem + L::QB)};
+      bool pending[2] = {false, false};
+      int pcount[2] = {0, 0};
+      mbar_wait(q_full, 0);
+      auto issue_pv = [&](int g, int jt) {
+        mbar_wait(&p_full[g], pcount[g] & 1);
+        ++pcount[g];
+        mbar_wait(&v_full[jt & 1], (jt >> 1) & 1);
+        tc_fence_after();
+        const uint32_t sv = smem_u32(smem + L::KV + (jt & 1) * 2 * Tile<D>::BYTES + Tile<D>::BYTES);
+        const uint32_t tP = tmem + 128 * g, tO = tmem + 256 + 128 * g;
+#pragma unroll
+        for (int kk = 0; kk < AT_TILE / 16; ++kk)
+          umma_f16_ts(tO, tP + kk * 8, mnmajor_desc(sv, kk), id_o, (jt > 0 || kk > 0));
+        pending[g] = false;
+      };
+      for (int j = 0; j < nkv; ++j) {
+        mbar_wait(&k_full[j & 1], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t sk = smem_u32(smem + L::KV + (j & 1) * 2 * Tile<D>::BYTES);
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+          if (pending[g]) issue_pv(g, j - 1);
+          if (j <= last[g]) {
+            const uint32_t tS = tmem + 128 * g;
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk)
+              umma_f16_ss(tS, kmajor_desc(sq[g], kk), kmajor_desc(sk, kk), id_s, kk > 0);
+            umma_commit(&s_full[g]);
+            pending[g] = true;
+          }
+        }
+        if (j > 0) umma_commit(&kv_empty[(j - 1) & 1]);
+      }
+      for (int g = 0; g < 2; ++g)
+        if (pending[g]) issue_pv(g, last[g]);
+      umma_commit(&o_full[0]);
+      umma_commit(&o_full[1]);
+    }
+  } else {
+    // ---------------- softmax warpgroups: thread = query row of tile g
+    const int g = warp >> 2;
+    const int quad = warp & 3;
+    if (g == 0 || has_b) {
+      const int r = quad * 32 + lane;
+      const int qt = qtile[g];
+      const int qrow = qt * AT_TILE + r;
+      const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+      const uint32_t tS = tmem + 128 * g + lane_off, tO = tmem + 256 + 128 * g + lane_off;
+      const float c = p.scale_log2;
+      float m_used = -INFINITY, l_run = 0.f;
+      for (int j = 0; j <= qt; ++j) {
+        mbar_wait(&s_full[g], j & 1);
+        tc_fence_after();
+        uint32_t raw[AT_TILE];
+#pragma unroll
+        for (int ch = 0; ch < AT_TILE / 32; ++ch)
+          tmem_ld32(tS + ch * 32, *reinterpret_cast<uint32_t(*)[32]>(raw + ch * 32));
+        tmem_wait_ld();
+        float mx = -INFINITY;
+        if (j == qt) {
+#pragma unroll
+          for (int i = 0; i < AT_TILE; ++i) {
+            if (i > r) raw[i] = __float_as_uint(-INFINITY);
+            mx = fmaxf(mx, __uint_as_float(raw[i]));
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < AT_TILE; ++i) mx = fmaxf(mx, __uint_as_float(raw[i]));
+        }
+        mx *= c;
+        const float m_new = (mx > m_used + 8.0f) ? mx : m_used;
+        const float alpha = fast_exp2(m_used - m_new);
+        if (j > 0 && __any_sync(0xffffffffu, m_new != m_used)) {
+#pragma unroll
+          for (int ch = 0; ch < D / 16; ++ch) {
+            uint32_t o16[16];
+            tmem_ld16(tO + ch * 16, o16);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o16[i] = __float_as_uint(__uint_as_float(o16[i]) * alpha);
+            tmem_st16(tO + ch * 16, o16);
+          }
+        }
+        m_used = m_new;
+        const float neg_m = -m_new;
+        float rs = 0.f;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          uint32_t pk[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float e0 = fast_exp2(fmaf(__uint_as_float(raw[half * 64 + 2 * i]), c, neg_m));
+            const float e1 = fast_exp2(fmaf(__uint_as_float(raw[half * 64 + 2 * i + 1]), c, neg_m));
+            rs += e0 + e1;
+            pk[i] = pack_bf16(e0, e1);
+          }
+          tmem_st32(tS + half * 32, pk);  // P over the first 64 columns of S
+        }
+        tmem_wait_st();
+        l_run = l_run * alpha + rs;
+        tc_fence_before();
+        mbar_arrive(&p_full[g]);
+      }
+      mbar_wait(&o_full[g], 0);
+      tc_fence_after();
+      const float inv_l = 1.f / l_run;
+      __nv_bfloat16* orow = p.o + (static_cast<int64_t>(qrow) * p.b + bi) * p.ld_o + head * D;
+#pragma unroll
+      for (int ch = 0; ch < D / 32; ++ch) {
+        uint32_t o32[32];
+        tmem_ld32(tO + ch * 32, o32);
+        tmem_wait_ld();
+        if (qrow < p.s) {
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            float f[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(o32[v * 8 + i]) * inv_l;
+            *reinterpret_cast<uint4*>(orow + ch * 32 + v * 8) =
+                make_uint4(pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]),
+                           pack_bf16(f[6], f[7]));
+          }
+        }
+      }
+      if (qrow < p.s) p.lse[static_cast<int64_t>(bh) * p.s + qrow] = (m_used + log2f(l_run)) * LN2;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// =====================================================================================
 // backward
 // =====================================================================================
 template <int D>
@@ -478,6 +704,679 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
   }
 }
 
+// =====================================================================================
+// backward v2
+// =====================================================================================
+//
+// CTA = one 128-row key tile of one (batch, head), walking query tiles diag..end.
+//   warps 0-7   compute: warpgroup g handles query columns [64g, 64g+64) of the
+//               transposed tiles; thread = key row.  P^T goes back into TMEM
+//               (A operand of dV += P^T dO), dS^T into a swizzled smem tile
+//               (A operand of dK += dS^T Q, and - read MN-major - of dQ = dS K).
+//   warps 8-11  dQ reduction: TMEM -> registers -> fp32 vector atomics, so the
+//               global reduction overlaps the next tile's MMAs and softmax.
+//   warp 12     TMA (K, V once; Q, dO double-buffered).
+//   warp 13     MMA issuer + TMEM owner.
+// TMEM: dK 0-127 | dV 128-255 | S^T (P^T in 256-287 / 320-351) 256-383 | dP^T = dQ 384-511.
+// MMA order per query tile i:  S^T(i), [dQ(i-1) read out] dP^T(i), [P^T(i)] dV,
+// [dS^T(i)] dK, dQ(i)  - so S^T(i+1) runs while the reducers drain dQ(i).
+
+constexpr int BWD2_THREADS = 448;
+
+template <int D>
+struct Bwd2Smem {
+  static constexpr int K = 0;
+  static constexpr int V = K + Tile<D>::BYTES;
+  static constexpr int Q = V + Tile<D>::BYTES;        // 2 stages
+  static constexpr int DO = Q + 2 * Tile<D>::BYTES;   // 2 stages
+  static constexpr int DST = DO + 2 * Tile<D>::BYTES;  // dS^T [kv x q], 2 atoms
+  static constexpr int STAT = DST + AT_TILE * AT_TILE * 2;  // [2 slots][lse2 | delta][128]
+  static constexpr int BAR = STAT + 2 * 2 * AT_TILE * 4;
+  static constexpr int TOTAL = BAR + 256;  // requires a 1024-aligned dynamic smem base
+};
+
+HX_DEVICE void named_barrier_sync(uint32_t id, uint32_t threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+template <int D>
+__global__ void __launch_bounds__(BWD2_THREADS, 1)
+    attn_bwd2_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                     const AttnParams p) {
+  using L = Bwd2Smem<D>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if ((smem_u32(smem) & 1023) != 0) __trap();
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR);
+  uint64_t* kv_full = bars;         // 1
+  uint64_t* qdo_full = bars + 1;    // 2
+  uint64_t* qdo_empty = bars + 3;   // 2
+  uint64_t* s_full = bars + 5;
+  uint64_t* dp_full = bars + 6;
+  uint64_t* p_full = bars + 7;      // 256 arrivals
+  uint64_t* ds_full = bars + 8;     // 256 arrivals
+  uint64_t* dq_full = bars + 9;
+  uint64_t* dq_free = bars + 10;    // 128 arrivals
+  uint64_t* acc_full = bars + 11;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  float* stat = reinterpret_cast<float*>(smem + L::STAT);
+
+  const int warp = warp_id(), lane = lane_id();
+  const int nq = (p.s + AT_TILE - 1) / AT_TILE;
+  const int kt = static_cast<int>(blockIdx.x);
+  const int bh = blockIdx.y;
+  const int bi = bh / p.heads, head = bh % p.heads;
+  const int qcol = head * D, kcol = p.h + head * D, vcol = 2 * p.h + head * D;
+  const int n_it = nq - kt;
+
+  if (warp == 12 && lane == 0) {
+    tma_prefetch(&tm_qkv);
+    tma_prefetch(&tm_do);
+    for (int i = 0; i < 12; ++i)
+      mbar_init(&bars[i], (i == 7 || i == 8) ? 256 : (i == 10 ? 128 : 1));
+    fence_barrier_init();
+  }
+  if (warp == 13) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tDK = tmem, tDV = tmem + 128, tS = tmem + 256, tDP = tmem + 384;
+
+  if (warp == 12) {
+    if (lane == 0) {  // ---------------- TMA producer
+      mbar_arrive_expect_tx(kv_full, 2 * Tile<D>::BYTES);
+      tma_tile<D>(smem + L::K, &tm_qkv, kv_full, kcol, bi, kt * AT_TILE);
+      tma_tile<D>(smem + L::V, &tm_qkv, kv_full, vcol, bi, kt * AT_TILE);
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it & 1, q0 = (kt + it) * AT_TILE;
+        mbar_wait(&qdo_empty[st], ((it >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&qdo_full[st], 2 * Tile<D>::BYTES);
+        tma_tile<D>(smem + L::Q + st * Tile<D>::BYTES, &tm_qkv, &qdo_full[st], qcol, bi, q0);
+        tma_tile<D>(smem + L::DO + st * Tile<D>::BYTES, &tm_do, &qdo_full[st], head * D, bi, q0);
+      }
+    }
+  } else if (warp == 13) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      constexpr uint32_t id_sp = idesc_bf16(128, 128, false, false);
+      constexpr uint32_t id_kv = idesc_bf16(128, D, false, true);
+      constexpr uint32_t id_q = idesc_bf16(128, D, true, true);
+      const uint32_t sk = smem_u32(smem + L::K), sv = smem_u32(smem + L::V);
+      const uint32_t sdst = smem_u32(smem + L::DST);
+      mbar_wait(kv_full, 0);
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it & 1;
+        const uint32_t sq = smem_u32(smem + L::Q + st * Tile<D>::BYTES);
+        const uint32_t sdo = smem_u32(smem + L::DO + st * Tile<D>::BYTES);
+        mbar_wait(&qdo_full[st], (it >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_f16_ss(tS, kmajor_desc(sk, kk), kmajor_desc(sq, kk), id_sp, kk > 0);
+        umma_commit(s_full);
+        if (it > 0) {
+          mbar_wait(dq_free, (it - 1) & 1);
+          tc_fence_after();
+        }
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_f16_ss(tDP, kmajor_desc(sv, kk), kmajor_desc(sdo, kk), id_sp, kk > 0);
+        umma_commit(dp_full);
+        mbar_wait(p_full, it & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < AT_TILE / 16; ++kk)  // P^T of warpgroup kk/4 at 256 + 64*(kk/4)
+          umma_f16_ts(tDV, tS + (kk >> 2) * 64 + (kk & 3) * 8, mnmajor_desc(sdo, kk), id_kv,
+                      it > 0 || kk > 0);
+        mbar_wait(ds_full, it & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < AT_TILE / 16; ++kk)
+          umma_f16_ss(tDK, kmajor_desc(sdst, kk), mnmajor_desc(sq, kk), id_kv, it > 0 || kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < AT_TILE / 16; ++kk)
+          umma_f16_ss(tDP, mnmajor_desc(sdst, kk), mnmajor_desc(sk, kk), id_q, kk > 0);
+        umma_commit(dq_full);
+        umma_commit(&qdo_empty[st]);
+      }
+      umma_commit(acc_full);
+    }
+  } else if (warp < 8) {
+    // ---------------- compute: thread = key row c, query columns [qoff, qoff+64)
+    const int g = warp >> 2, quad = warp & 3;
+    const int c = quad * 32 + lane;
+    const int qoff = 64 * g;
+    const int ct = threadIdx.x;  // 0..255
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const int64_t row_base = static_cast<int64_t>(bh) * p.s;
+    uint8_t* dst = smem + L::DST;
+    for (int it = 0; it < n_it; ++it) {
+      const int qtile = kt + it, q0 = qtile * AT_TILE;
+      float* s_lse = stat + (it & 1) * 2 * AT_TILE;
+      float* s_del = s_lse + AT_TILE;
+      {
+        const int qi = ct & (AT_TILE - 1);
+        const int q = q0 + qi;
+        if (ct < AT_TILE) s_lse[qi] = q < p.s ? p.lse[row_base + q] * LOG2E : 0.f;
+        else s_del[qi] = q < p.s ? p.delta[row_base + q] : 0.f;
+      }
+      named_barrier_sync(1, 256);
+      const bool diag = (qtile == kt);
+      mbar_wait(s_full, it & 1);
+      tc_fence_after();
+      uint32_t raw[64];
+      tmem_ld32(tS + lane_off + qoff, *reinterpret_cast<uint32_t(*)[32]>(raw));
+      tmem_ld32(tS + lane_off + qoff + 32, *reinterpret_cast<uint32_t(*)[32]>(raw + 32));
+      tmem_wait_ld();
+      float pv[64];
+#pragma unroll
+      for (int j = 0; j < 64; ++j) {
+        const int qi = qoff + j;
+        float pr = fast_exp2(fmaf(__uint_as_float(raw[j]), p.scale_log2, -s_lse[qi]));
+        if ((diag && qi < c) || q0 + qi >= p.s) pr = 0.f;
+        pv[j] = pr;
+      }
+      {
+        uint32_t pk[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) pk[j] = pack_bf16(pv[2 * j], pv[2 * j + 1]);
+        tmem_st32(tS + lane_off + qoff, pk);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(p_full);
+      mbar_wait(dp_full, it & 1);
+      tc_fence_after();
+      tmem_ld32(tDP + lane_off + qoff, *reinterpret_cast<uint32_t(*)[32]>(raw));
+      tmem_ld32(tDP + lane_off + qoff + 32, *reinterpret_cast<uint32_t(*)[32]>(raw + 32));
+      tmem_wait_ld();
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        float ds[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int j = v * 8 + i;
+          ds[i] = pv[j] * (__uint_as_float(raw[j]) - s_del[qoff + j]);
+        }
+        *reinterpret_cast<uint4*>(dst + swz_off(c, qoff + v * 8)) =
+            make_uint4(pack_bf16(ds[0], ds[1]), pack_bf16(ds[2], ds[3]), pack_bf16(ds[4], ds[5]),
+                       pack_bf16(ds[6], ds[7]));
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(ds_full);
+    }
+    // dK, dV epilogue (rows c, columns [64g, 64g+64))
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    const int krow = kt * AT_TILE + c;
+    const int64_t tok = static_cast<int64_t>(krow) * p.b + bi;
+    __nv_bfloat16* dk = p.dqkv + tok * p.ld_dqkv + p.h + head * D;
+    __nv_bfloat16* dv = p.dqkv + tok * p.ld_dqkv + 2 * p.h + head * D;
+#pragma unroll
+    for (int ch = 0; ch < D / 64; ++ch) {
+      const int col = g * (D / 2) + ch * 32;
+      if (col >= (g + 1) * (D / 2)) break;
+      uint32_t rk[32], rv[32];
+      tmem_ld32(tDK + lane_off + col, rk);
+      tmem_ld32(tDV + lane_off + col, rv);
+      tmem_wait_ld();
+      if (krow < p.s) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          float fk[8], fv[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            fk[i] = __uint_as_float(rk[v * 8 + i]) * p.scale;
+            fv[i] = __uint_as_float(rv[v * 8 + i]);
+          }
+          *reinterpret_cast<uint4*>(dk + col + v * 8) =
+              make_uint4(pack_bf16(fk[0], fk[1]), pack_bf16(fk[2], fk[3]), pack_bf16(fk[4], fk[5]), pack_bf16(fk[6], fk[7]));
+          *reinterpret_cast<uint4*>(dv + col + v * 8) =
+              make_uint4(pack_bf16(fv[0], fv[1]), pack_bf16(fv[2], fv[3]), pack_bf16(fv[4], fv[5]), pack_bf16(fv[6], fv[7]));
+        }
+      }
+    }
+  } else {
+    // ---------------- dQ reducers (warps 8-11): thread = query row
+    const int quad = warp & 3;
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const int64_t row_base = static_cast<int64_t>(bh) * p.s;
+    for (int it = 0; it < n_it; ++it) {
+      const int q = (kt + it) * AT_TILE + quad * 32 + lane;
+      mbar_wait(dq_full, it & 1);
+      tc_fence_after();
+      float* dq = p.dq_acc + (row_base + q) * D;
+#pragma unroll
+      for (int half = 0; half < D / 64; ++half) {
+        uint32_t r0[32], r1[32];
+        tmem_ld32(tDP + lane_off + half * 64, r0);
+        tmem_ld32(tDP + lane_off + half * 64 + 32, r1);
+        tmem_wait_ld();
+        if (half == D / 64 - 1) {
+          tc_fence_before();
+          mbar_arrive(dq_free);
+        }
+        if (q < p.s) {
+#pragma unroll
+          for (int v = 0; v < 8; ++v)
+            atomicAdd(reinterpret_cast<float4*>(dq + half * 64 + 4 * v),
+                      make_float4(__uint_as_float(r0[4 * v]) * p.scale, __uint_as_float(r0[4 * v + 1]) * p.scale,
+                                  __uint_as_float(r0[4 * v + 2]) * p.scale, __uint_as_float(r0[4 * v + 3]) * p.scale));
+#pragma unroll
+          for (int v = 0; v < 8; ++v)
+            atomicAdd(reinterpret_cast<float4*>(dq + half * 64 + 32 + 4 * v),
+                      make_float4(__uint_as_float(r1[4 * v]) * p.scale, __uint_as_float(r1[4 * v + 1]) * p.scale,
+                                  __uint_as_float(r1[4 * v + 2]) * p.scale, __uint_as_float(r1[4 * v + 3]) * p.scale));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 13) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// =====================================================================================
+// backward v3: atomic-free split into a dK/dV kernel and a dQ kernel
+// =====================================================================================
+//
+// dK/dV kernel: CTA = one 128-row key tile, walks query tiles diag..end.
+//   MMA order per query tile i: S^T(i), dP^T(i), [P^T(i) in TMEM] dV += P^T dO,
+//   [dS^T(i) in smem] dK += dS^T Q; S^T(i+1) follows immediately (P^T(i) was
+//   consumed by dV(i) earlier in the same in-order MMA stream).
+//   TMEM: dK 0-127 | dV 128-255 | S^T (P^T at 256+64g) 256-383 | dP^T 384-511.
+// dQ kernel: CTA = one 128-row query tile, walks key tiles 0..diag.
+//   S(j) double-buffered in TMEM so S(j+1) overlaps the softmax of tile j;
+//   dQ accumulates in TMEM across all key tiles and is written once as bf16.
+//   TMEM: S0 0-127 | S1 128-255 | dP 256-383 | dQ 384-511.
+// Both: warps 0-7 compute (warpgroup g owns columns [64g, 64g+64) of the
+// 128-wide score tiles, thread = TMEM lane = row), warp 8 TMA, warp 9 MMA.
+
+constexpr int BWD3_THREADS = 320;
+
+template <int D>
+struct KVSmem {
+  static constexpr int K = 0;
+  static constexpr int V = K + Tile<D>::BYTES;
+  static constexpr int Q = V + Tile<D>::BYTES;        // 2 stages
+  static constexpr int DO = Q + 2 * Tile<D>::BYTES;   // 2 stages
+  static constexpr int DST = DO + 2 * Tile<D>::BYTES;  // dS^T [kv x q]
+  static constexpr int STAT = DST + AT_TILE * AT_TILE * 2;  // [2 slots][lse2 | delta][128]
+  static constexpr int BAR = STAT + 2 * 2 * AT_TILE * 4;
+  static constexpr int TOTAL = BAR + 256;
+};
+
+template <int D>
+__global__ void __launch_bounds__(BWD3_THREADS, 1)
+    attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                         const AttnParams p) {
+  using L = KVSmem<D>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if ((smem_u32(smem) & 1023) != 0) __trap();
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR);
+  uint64_t* kv_full = bars;        // 1
+  uint64_t* qdo_full = bars + 1;   // 2
+  uint64_t* qdo_empty = bars + 3;  // 2
+  uint64_t* s_full = bars + 5;
+  uint64_t* dp_full = bars + 6;
+  uint64_t* p_full = bars + 7;     // 256 arrivals
+  uint64_t* ds_full = bars + 8;    // 256 arrivals
+  uint64_t* acc_full = bars + 9;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+  float* stat = reinterpret_cast<float*>(smem + L::STAT);
+
+  const int warp = warp_id(), lane = lane_id();
+  const int nq = (p.s + AT_TILE - 1) / AT_TILE;
+  const int kt = static_cast<int>(blockIdx.x);
+  const int bh = blockIdx.y;
+  const int bi = bh / p.heads, head = bh % p.heads;
+  const int qcol = head * D, kcol = p.h + head * D, vcol = 2 * p.h + head * D;
+  const int n_it = nq - kt;
+
+  if (warp == 8 && lane == 0) {
+    tma_prefetch(&tm_qkv);
+    tma_prefetch(&tm_do);
+    for (int i = 0; i < 10; ++i) mbar_init(&bars[i], (i == 7 || i == 8) ? 256 : 1);
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tDK = tmem, tDV = tmem + 128, tS = tmem + 256, tDP = tmem + 384;
+
+  if (warp == 8) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(kv_full, 2 * Tile<D>::BYTES);
+      tma_tile<D>(smem + L::K, &tm_qkv, kv_full, kcol, bi, kt * AT_TILE);
+      tma_tile<D>(smem + L::V, &tm_qkv, kv_full, vcol, bi, kt * AT_TILE);
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it & 1, q0 = (kt + it) * AT_TILE;
+        mbar_wait(&qdo_empty[st], ((it >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&qdo_full[st], 2 * Tile<D>::BYTES);
+        tma_tile<D>(smem + L::Q + st * Tile<D>::BYTES, &tm_qkv, &qdo_full[st], qcol, bi, q0);
+        tma_tile<D>(smem + L::DO + st * Tile<D>::BYTES, &tm_do, &qdo_full[st], head * D, bi, q0);
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {
+      constexpr uint32_t id_sp = idesc_bf16(128, 128, false, false);
+      constexpr uint32_t id_kv = idesc_bf16(128, D, false, true);
+      const uint32_t sk = smem_u32(smem + L::K), sv = smem_u32(smem + L::V);
+      const uint32_t sdst = smem_u32(smem + L::DST);
+      mbar_wait(kv_full, 0);
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it & 1;
+        const uint32_t sq = smem_u32(smem + L::Q + st * Tile<D>::BYTES);
+        const uint32_t sdo = smem_u32(smem + L::DO + st * Tile<D>::BYTES);
+        mbar_wait(&qdo_full[st], (it >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_f16_ss(tS, kmajor_desc(sk, kk), kmajor_desc(sq, kk), id_sp, kk > 0);
+        umma_commit(s_full);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_f16_ss(tDP, kmajor_desc(sv, kk), kmajor_desc(sdo, kk), id_sp, kk > 0);
+        umma_commit(dp_full);
+        mbar_wait(p_full, it & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < AT_TILE / 16; ++kk)
+          umma_f16_ts(tDV, tS + (kk >> 2) * 64 + (kk & 3) * 8, mnmajor_desc(sdo, kk), id_kv,
+                      it > 0 || kk > 0);
+        mbar_wait(ds_full, it & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < AT_TILE / 16; ++kk)
+          umma_f16_ss(tDK, kmajor_desc(sdst, kk), mnmajor_desc(sq, kk), id_kv, it > 0 || kk > 0);
+        umma_commit(&qdo_empty[st]);
+      }
+      umma_commit(acc_full);
+    }
+  } else {
+    const int g = warp >> 2, quad = warp & 3;
+    const int c = quad * 32 + lane;
+    const int qoff = 64 * g;
+    const int ct = threadIdx.x;
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const int64_t row_base = static_cast<int64_t>(bh) * p.s;
+    uint8_t* dst = smem + L::DST;
+    for (int it = 0; it < n_it; ++it) {
+      const int qtile = kt + it, q0 = qtile * AT_TILE;
+      float* s_lse = stat + (it & 1) * 2 * AT_TILE;
+      float* s_del = s_lse + AT_TILE;
+      {
+        const int qi = ct & (AT_TILE - 1);
+        const int q = q0 + qi;
+        if (ct < AT_TILE) s_lse[qi] = q < p.s ? p.lse[row_base + q] * LOG2E : 0.f;
+        else s_del[qi] = q < p.s ? p.delta[row_base + q] : 0.f;
+      }
+      named_barrier_sync(1, 256);
+      const bool diag = (qtile == kt);
+      mbar_wait(s_full, it & 1);
+      tc_fence_after();
+      uint32_t raw[64];
+      tmem_ld32(tS + lane_off + qoff, *reinterpret_cast<uint32_t(*)[32]>(raw));
+      tmem_ld32(tS + lane_off + qoff + 32, *reinterpret_cast<uint32_t(*)[32]>(raw + 32));
+      tmem_wait_ld();
+      uint32_t pk[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int qi = qoff + 2 * j;
+        float p0 = fast_exp2(fmaf(__uint_as_float(raw[2 * j]), p.scale_log2, -s_lse[qi]));
+        float p1 = fast_exp2(fmaf(__uint_as_float(raw[2 * j + 1]), p.scale_log2, -s_lse[qi + 1]));
+        if ((diag && qi < c) || q0 + qi >= p.s) p0 = 0.f;
+        if ((diag && qi + 1 < c) || q0 + qi + 1 >= p.s) p1 = 0.f;
+        pk[j] = pack_bf16(p0, p1);
+      }
+      tmem_st32(tS + lane_off + qoff, pk);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(p_full);
+      mbar_wait(dp_full, it & 1);
+      tc_fence_after();
+      tmem_ld32(tDP + lane_off + qoff, *reinterpret_cast<uint32_t(*)[32]>(raw));
+      tmem_ld32(tDP + lane_off + qoff + 32, *reinterpret_cast<uint32_t(*)[32]>(raw + 32));
+      tmem_wait_ld();
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        uint32_t w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int j = v * 4 + i;  // packed pair index
+          const float2 pp = unpack_bf16(pk[j]);
+          const int qi = qoff + 2 * j;
+          w[i] = pack_bf16(pp.x * (__uint_as_float(raw[2 * j]) - s_del[qi]),
+                           pp.y * (__uint_as_float(raw[2 * j + 1]) - s_del[qi + 1]));
+        }
+        *reinterpret_cast<uint4*>(dst + swz_off(c, qoff + v * 8)) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(ds_full);
+    }
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    const int krow = kt * AT_TILE + c;
+    const int64_t tok = static_cast<int64_t>(krow) * p.b + bi;
+    __nv_bfloat16* dk = p.dqkv + tok * p.ld_dqkv + p.h + head * D;
+    __nv_bfloat16* dv = p.dqkv + tok * p.ld_dqkv + 2 * p.h + head * D;
+#pragma unroll
+    for (int ch = 0; ch < D / 64; ++ch) {
+      const int col = g * (D / 2) + ch * 32;
+      uint32_t rk[32], rv[32];
+      tmem_ld32(tDK + lane_off + col, rk);
+      tmem_ld32(tDV + lane_off + col, rv);
+      tmem_wait_ld();
+      if (krow < p.s) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          float fk[8], fv[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            fk[i] = __uint_as_float(rk[v * 8 + i]) * p.scale;
+            fv[i] = __uint_as_float(rv[v * 8 + i]);
+          }
+          *reinterpret_cast<uint4*>(dk + col + v * 8) =
+              make_uint4(pack_bf16(fk[0], fk[1]), pack_bf16(fk[2], fk[3]), pack_bf16(fk[4], fk[5]), pack_bf16(fk[6], fk[7]));
+          *reinterpret_cast<uint4*>(dv + col + v * 8) =
+              make_uint4(pack_bf16(fv[0], fv[1]), pack_bf16(fv[2], fv[3]), pack_bf16(fv[4], fv[5]), pack_bf16(fv[6], fv[7]));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+template <int D>
+struct QSmem {
+  static constexpr int Q = 0;
+  static constexpr int DO = Q + Tile<D>::BYTES;
+  static constexpr int KV = DO + Tile<D>::BYTES;          // 2 stages x (K, V)
+  static constexpr int DS = KV + 4 * Tile<D>::BYTES;       // dS [q x kv]
+  static constexpr int BAR = DS + AT_TILE * AT_TILE * 2;
+  static constexpr int TOTAL = BAR + 256;
+};
+
+template <int D>
+__global__ void __launch_bounds__(BWD3_THREADS, 1)
+    attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                       const AttnParams p) {
+  using L = QSmem<D>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if ((smem_u32(smem) & 1023) != 0) __trap();
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR);
+  uint64_t* q_full = bars;          // 1
+  uint64_t* kv_full = bars + 1;     // 2
+  uint64_t* kv_empty = bars + 3;    // 2
+  uint64_t* s_full = bars + 5;      // 2
+  uint64_t* s_free = bars + 7;      // 2, 256 arrivals
+  uint64_t* dp_full = bars + 9;
+  uint64_t* ds_full = bars + 10;    // 256 arrivals
+  uint64_t* dq_done = bars + 11;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+
+  const int warp = warp_id(), lane = lane_id();
+  const int nq = (p.s + AT_TILE - 1) / AT_TILE;
+  const int qt = nq - 1 - static_cast<int>(blockIdx.x);
+  const int nkv = qt + 1;
+  const int bh = blockIdx.y;
+  const int bi = bh / p.heads, head = bh % p.heads;
+  const int qcol = head * D, kcol = p.h + head * D, vcol = 2 * p.h + head * D;
+
+  if (warp == 8 && lane == 0) {
+    tma_prefetch(&tm_qkv);
+    tma_prefetch(&tm_do);
+    for (int i = 0; i < 12; ++i)
+      mbar_init(&bars[i], (i == 7 || i == 8 || i == 10) ? 256 : 1);
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tDP = tmem + 256, tDQ = tmem + 384;
+
+  if (warp == 8) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(q_full, 2 * Tile<D>::BYTES);
+      tma_tile<D>(smem + L::Q, &tm_qkv, q_full, qcol, bi, qt * AT_TILE);
+      tma_tile<D>(smem + L::DO, &tm_do, q_full, head * D, bi, qt * AT_TILE);
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j & 1;
+        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        uint8_t* kb = smem + L::KV + st * 2 * Tile<D>::BYTES;
+        mbar_arrive_expect_tx(&kv_full[st], 2 * Tile<D>::BYTES);
+        tma_tile<D>(kb, &tm_qkv, &kv_full[st], kcol, bi, j * AT_TILE);
+        tma_tile<D>(kb + Tile<D>::BYTES, &tm_qkv, &kv_full[st], vcol, bi, j * AT_TILE);
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {
+      constexpr uint32_t id_sp = idesc_bf16(128, 128, false, false);
+      constexpr uint32_t id_q = idesc_bf16(128, D, false, true);
+      const uint32_t sq = smem_u32(smem + L::Q), sdo = smem_u32(smem + L::DO);
+      const uint32_t sds = smem_u32(smem + L::DS);
+      auto sk = [&](int j) { return smem_u32(smem + L::KV + (j & 1) * 2 * Tile<D>::BYTES); };
+      auto issue_s = [&](int j) {
+        mbar_wait(&kv_full[j & 1], (j >> 1) & 1);
+        if (j >= 2) mbar_wait(&s_free[j & 1], ((j >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t ts = tmem + (j & 1) * 128;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_f16_ss(ts, kmajor_desc(sq, kk), kmajor_desc(sk(j), kk), id_sp, kk > 0);
+        umma_commit(&s_full[j & 1]);
+      };
+      auto issue_dp = [&](int j) {
+        const uint32_t sv = sk(j) + Tile<D>::BYTES;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_f16_ss(tDP, kmajor_desc(sdo, kk), kmajor_desc(sv, kk), id_sp, kk > 0);
+        umma_commit(dp_full);
+      };
+      mbar_wait(q_full, 0);
+      issue_s(0);
+      issue_dp(0);
+      for (int j = 0; j < nkv; ++j) {
+        if (j + 1 < nkv) issue_s(j + 1);
+        mbar_wait(ds_full, j & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < AT_TILE / 16; ++kk)
+          umma_f16_ss(tDQ, kmajor_desc(sds, kk), mnmajor_desc(sk(j), kk), id_q, j > 0 || kk > 0);
+        umma_commit(&kv_empty[j & 1]);
+        if (j + 1 < nkv) issue_dp(j + 1);
+      }
+      umma_commit(dq_done);
+    }
+  } else {
+    // compute: thread = query row r; warpgroup g owns key columns [64g, 64g+64)
+    const int g = warp >> 2, quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const int koff = 64 * g;
+    const int q = qt * AT_TILE + r;
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const int64_t row = static_cast<int64_t>(bh) * p.s + q;
+    const float lse2 = q < p.s ? p.lse[row] * LOG2E : 0.f;
+    const float dlt = q < p.s ? p.delta[row] : 0.f;
+    uint8_t* ds_s = smem + L::DS;
+    for (int j = 0; j < nkv; ++j) {
+      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t raw[64];
+      const uint32_t ts = tmem + (j & 1) * 128 + lane_off + koff;
+      tmem_ld32(ts, *reinterpret_cast<uint32_t(*)[32]>(raw));
+      tmem_ld32(ts + 32, *reinterpret_cast<uint32_t(*)[32]>(raw + 32));
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&s_free[j & 1]);
+      const bool diag = (j == qt);
+      float pv[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        float pr = fast_exp2(fmaf(__uint_as_float(raw[i]), p.scale_log2, -lse2));
+        if (diag && koff + i > r) pr = 0.f;
+        pv[i] = pr;
+      }
+      mbar_wait(dp_full, j & 1);
+      tc_fence_after();
+      tmem_ld32(tDP + lane_off + koff, *reinterpret_cast<uint32_t(*)[32]>(raw));
+      tmem_ld32(tDP + lane_off + koff + 32, *reinterpret_cast<uint32_t(*)[32]>(raw + 32));
+      tmem_wait_ld();
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        float ds[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) ds[i] = pv[v * 8 + i] * (__uint_as_float(raw[v * 8 + i]) - dlt);
+        *reinterpret_cast<uint4*>(ds_s + swz_off(r, koff + v * 8)) =
+            make_uint4(pack_bf16(ds[0], ds[1]), pack_bf16(ds[2], ds[3]), pack_bf16(ds[4], ds[5]),
+                       pack_bf16(ds[6], ds[7]));
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(ds_full);
+    }
+    mbar_wait(dq_done, 0);
+    tc_fence_after();
+    __nv_bfloat16* dqp = p.dqkv + (static_cast<int64_t>(q) * p.b + bi) * p.ld_dqkv + head * D;
+#pragma unroll
+    for (int ch = 0; ch < D / 64; ++ch) {
+      const int col = g * (D / 2) + ch * 32;
+      uint32_t rq[32];
+      tmem_ld32(tDQ + lane_off + col, rq);
+      tmem_wait_ld();
+      if (q < p.s) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          float f[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(rq[v * 8 + i]) * p.scale;
+          *reinterpret_cast<uint4*>(dqp + col + v * 8) =
+              make_uint4(pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]), pack_bf16(f[6], f[7]));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 // D = rowsum(dO * O) per (batch, head, query); also zeroes the dQ accumulator.
 template <int D>
 __global__ void __launch_bounds__(256) attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ o,
@@ -509,8 +1408,10 @@ __global__ void __launch_bounds__(256) attn_bwd_pre_kernel(const __nv_bfloat16* 
       const int head = v / VPH, sub = v % VPH;
       const int64_t row = (static_cast<int64_t>(bi) * heads + head) * s + si;
       if (sub == 0) delta[row] = acc;
-      reinterpret_cast<uint4*>(dq_acc + row * D)[sub * 2] = make_uint4(0, 0, 0, 0);
-      reinterpret_cast<uint4*>(dq_acc + row * D)[sub * 2 + 1] = make_uint4(0, 0, 0, 0);
+      if (dq_acc) {
+        reinterpret_cast<uint4*>(dq_acc + row * D)[sub * 2] = make_uint4(0, 0, 0, 0);
+        reinterpret_cast<uint4*>(dq_acc + row * D)[sub * 2 + 1] = make_uint4(0, 0, 0, 0);
+      }
     }
   }
 }
@@ -547,15 +1448,23 @@ static cudaError_t fwd_launch(const void* qkv, int ld_qkv, const AttnParams& p, 
   CUtensorMap tm;
   cudaError_t e = make_qkv_map(&tm, qkv, p.s, p.b, 3 * p.h, ld_qkv);
   if (e != cudaSuccess) return e;
-  auto k = attn_fwd_kernel<D>;
+  static const bool v1 = getenv("HX_ATTN_FWD_V1") != nullptr;
   static bool cfg = false;
   if (!cfg) {
-    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdSmem<D>::TOTAL);
+    e = cudaFuncSetAttribute(attn_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             FwdSmem<D>::TOTAL);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(attn_fwd2_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               Fwd2Smem<D>::TOTAL);
     if (e != cudaSuccess) return e;
     cfg = true;
   }
-  dim3 grid((p.s + AT_TILE - 1) / AT_TILE, p.b * p.heads);
-  k<<<grid, AT_THREADS, FwdSmem<D>::TOTAL, st>>>(tm, p);
+  const int nq = (p.s + AT_TILE - 1) / AT_TILE;
+  if (v1) {
+    attn_fwd_kernel<D><<<dim3(nq, p.b * p.heads), AT_THREADS, FwdSmem<D>::TOTAL, st>>>(tm, p);
+  } else {
+    attn_fwd2_kernel<D><<<dim3((nq + 1) / 2, p.b * p.heads), FWD2_THREADS, Fwd2Smem<D>::TOTAL, st>>>(tm, p);
+  }
   return cudaGetLastError();
 }
 
@@ -568,18 +1477,37 @@ static cudaError_t bwd_launch(const void* qkv, int ld_qkv, const void* o, const 
   e = make_qkv_map(&tdo, d_o, p.s, p.b, p.h, ld_o);
   if (e != cudaSuccess) return e;
   const int tokens = p.s * p.b;
-  attn_bwd_pre_kernel<D><<<(tokens + 7) / 8, 256, 0, st>>>(
-      static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(d_o), ld_o,
-      const_cast<float*>(p.delta), p.dq_acc, p.s, p.b, p.heads);
-  auto k = attn_bwd_kernel<D>;
+  // HX_ATTN_BWD=1 / 2: the earlier single-kernel variants with dQ atomics (kept for A/B runs)
+  static const int variant = getenv("HX_ATTN_BWD") ? atoi(getenv("HX_ATTN_BWD")) : 3;
   static bool cfg = false;
   if (!cfg) {
-    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdSmem<D>::TOTAL);
+    e = cudaFuncSetAttribute(attn_bwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdSmem<D>::TOTAL);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(attn_bwd2_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Bwd2Smem<D>::TOTAL);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(attn_bwd_dkdv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, KVSmem<D>::TOTAL);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(attn_bwd_dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, QSmem<D>::TOTAL);
     if (e != cudaSuccess) return e;
     cfg = true;
   }
-  dim3 grid((p.s + AT_TILE - 1) / AT_TILE, p.b * p.heads);
-  k<<<grid, AT_THREADS, BwdSmem<D>::TOTAL, st>>>(tq, tdo, p);
+  const bool atomics = variant != 3;
+  attn_bwd_pre_kernel<D><<<(tokens + 7) / 8, 256, 0, st>>>(
+      static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(d_o), ld_o,
+      const_cast<float*>(p.delta), atomics ? p.dq_acc : nullptr, p.s, p.b, p.heads);
+  const int nq = (p.s + AT_TILE - 1) / AT_TILE;
+  dim3 grid(nq, p.b * p.heads);
+  if (!atomics) {
+    attn_bwd_dkdv_kernel<D><<<grid, BWD3_THREADS, KVSmem<D>::TOTAL, st>>>(tq, tdo, p);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    attn_bwd_dq_kernel<D><<<grid, BWD3_THREADS, QSmem<D>::TOTAL, st>>>(tq, tdo, p);
+    return cudaGetLastError();
+  }
+  if (variant == 1)
+    attn_bwd_kernel<D><<<grid, AT_THREADS, BwdSmem<D>::TOTAL, st>>>(tq, tdo, p);
+  else
+    attn_bwd2_kernel<D><<<grid, BWD2_THREADS, Bwd2Smem<D>::TOTAL, st>>>(tq, tdo, p);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int64_t n8 = static_cast<int64_t>(tokens) * p.heads * D / 8;

@@ -1377,6 +1377,604 @@ __global__ void __launch_bounds__(BWD3_THREADS, 1)
   }
 }
 
+// =====================================================================================
+// backward v4: split kernels with a 64-wide streamed tile, double-buffered S/dP
+// =====================================================================================
+//
+// Halving the streamed tile (query tile in dK/dV, key tile in dQ) to 64 lets both
+// score tiles (S and dP) be double-buffered in TMEM next to the two 128-column
+// accumulators, so the tensor core computes S/dP of tile i+1 while the compute
+// warps turn tile i into P and dS.  N=64 MMAs keep the per-FLOP rate of N=128.
+//
+// dK/dV: TMEM dK 0-127 | dV 128-255 | S^T[b] 256+64b (P^T in its first 32 cols,
+//        16 per warpgroup) | dP^T[b] 384+64b.   smem: K, V (128 rows), Q / dO
+//        (64 rows, 3 stages), dS^T [128 x 64] x 2.
+// dQ:    TMEM S[b] 64b | dP[b] 128+64b | dQ 256-383.   smem: Q, dO (128 rows),
+//        K / V (64 rows, 3 stages), dS [128 x 64] x 2.
+constexpr int BT = 64;        // streamed tile
+constexpr int BT_STAGES = 3;
+
+template <int D>
+struct Half {  // [64 rows x D] tile
+  static constexpr int BYTES = BT * D * 2;
+};
+
+// K-major / MN-major descriptors for tiles with `rows` rows (atom = rows*128 bytes).
+HX_DEVICE uint64_t kdesc(uint32_t base, int kk, int rows) {
+  return sw128_desc(base + (kk >> 2) * rows * 128 + (kk & 3) * 32, 16, 1024);
+}
+HX_DEVICE uint64_t mndesc(uint32_t base, int kk, int rows) {
+  return sw128_desc(base + kk * 2048, rows * 128, 1024);
+}
+template <int D>
+HX_DEVICE void tma_tile_rows(void* dst, const CUtensorMap* map, uint64_t* bar, int col0, int bi, int s0, int rows) {
+#pragma unroll
+  for (int a = 0; a < D / 64; ++a)
+    tma_load_3d(static_cast<uint8_t*>(dst) + a * rows * 128, map, bar, col0 + 64 * a, bi, s0);
+}
+// 64-row swizzled tile: byte offset of 16-byte chunk (row, col), col < 64.
+HX_DEVICE uint32_t swz64(int row, int col) { return row * 128 + ((((col >> 3) & 7) ^ (row & 7)) << 4); }
+
+constexpr int BWD4_THREADS = 320;
+
+template <int D>
+struct KV4Smem {
+  static constexpr int K = 0;
+  static constexpr int V = K + Tile<D>::BYTES;
+  static constexpr int Q = V + Tile<D>::BYTES;              // BT_STAGES x [64 x D]
+  static constexpr int DO = Q + BT_STAGES * Half<D>::BYTES;  // BT_STAGES x [64 x D]
+  static constexpr int DST = DO + BT_STAGES * Half<D>::BYTES;  // 2 x [128 x 64]
+  static constexpr int STAT = DST + 2 * AT_TILE * BT * 2;     // [2][lse2 | delta][64]
+  static constexpr int BAR = STAT + 2 * 2 * BT * 4;
+  static constexpr int TOTAL = BAR + 256;
+};
+
+template <int D>
+__global__ void __launch_bounds__(BWD4_THREADS, 1)
+    attn_bwd_dkdv4_kernel(const __grid_constant__ CUtensorMap tm_qkv128, const __grid_constant__ CUtensorMap tm_qkv64,
+                          const __grid_constant__ CUtensorMap tm_do64, const AttnParams p) {
+  using L = KV4Smem<D>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if ((smem_u32(smem) & 1023) != 0) __trap();
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR);
+  uint64_t* kv_full = bars;                  // 1
+  uint64_t* qdo_full = bars + 1;             // BT_STAGES
+  uint64_t* qdo_empty = bars + 4;            // BT_STAGES
+  uint64_t* sdp_full = bars + 7;             // 2
+  uint64_t* p_full = bars + 9;               // 256 arrivals
+  uint64_t* ds_full = bars + 10;             // 256 arrivals
+  uint64_t* acc_full = bars + 11;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  float* stat = reinterpret_cast<float*>(smem + L::STAT);
+
+  const int warp = warp_id(), lane = lane_id();
+  const int nq = (p.s + BT - 1) / BT;           // 64-row query tiles
+  const int kt = static_cast<int>(blockIdx.x);  // 128-row key tile
+  const int bh = blockIdx.y;
+  const int bi = bh / p.heads, head = bh % p.heads;
+  const int qcol = head * D, kcol = p.h + head * D, vcol = 2 * p.h + head * D;
+  const int q_first = 2 * kt;                   // first query tile touching the diagonal
+  const int n_it = nq - q_first;
+
+  if (warp == 8 && lane == 0) {
+    tma_prefetch(&tm_qkv128);
+    tma_prefetch(&tm_qkv64);
+    tma_prefetch(&tm_do64);
+    for (int i = 0; i < 12; ++i) mbar_init(&bars[i], (i == 9 || i == 10) ? 256 : 1);
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tDK = tmem, tDV = tmem + 128, tS0 = tmem + 256, tDP0 = tmem + 384;
+
+  if (warp == 8) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(kv_full, 2 * Tile<D>::BYTES);
+      tma_tile_rows<D>(smem + L::K, &tm_qkv128, kv_full, kcol, bi, kt * AT_TILE, AT_TILE);
+      tma_tile_rows<D>(smem + L::V, &tm_qkv128, kv_full, vcol, bi, kt * AT_TILE, AT_TILE);
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it % BT_STAGES, q0 = (q_first + it) * BT;
+        mbar_wait(&qdo_empty[st], ((it / BT_STAGES) & 1) ^ 1);
+        mbar_arrive_expect_tx(&qdo_full[st], 2 * Half<D>::BYTES);
+        tma_tile_rows<D>(smem + L::Q + st * Half<D>::BYTES, &tm_qkv64, &qdo_full[st], qcol, bi, q0, BT);
+        tma_tile_rows<D>(smem + L::DO + st * Half<D>::BYTES, &tm_do64, &qdo_full[st], head * D, bi, q0, BT);
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {
+      constexpr uint32_t id_sp = idesc_bf16(128, BT, false, false);  // S^T, dP^T: M=128 kv, N=64 q
+      constexpr uint32_t id_kv = idesc_bf16(128, D, false, true);    // dV, dK
+      const uint32_t sk = smem_u32(smem + L::K), sv = smem_u32(smem + L::V);
+      auto issue_sdp = [&](int it) {
+        const int st = it % BT_STAGES, b = it & 1;
+        mbar_wait(&qdo_full[st], (it / BT_STAGES) & 1);
+        tc_fence_after();
+        const uint32_t sq = smem_u32(smem + L::Q + st * Half<D>::BYTES);
+        const uint32_t sdo = smem_u32(smem + L::DO + st * Half<D>::BYTES);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_f16_ss(tS0 + 64 * b, kdesc(sk, kk, AT_TILE), kdesc(sq, kk, BT), id_sp, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_f16_ss(tDP0 + 64 * b, kdesc(sv, kk, AT_TILE), kdesc(sdo, kk, BT), id_sp, kk > 0);
+        umma_commit(&sdp_full[b]);
+      };
+      mbar_wait(kv_full, 0);
+      issue_sdp(0);
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it % BT_STAGES, b = it & 1;
+        if (it + 1 < n_it) issue_sdp(it + 1);
+        const uint32_t sq = smem_u32(smem + L::Q + st * Half<D>::BYTES);
+        const uint32_t sdo = smem_u32(smem + L::DO + st * Half<D>::BYTES);
+        const uint32_t sdst = smem_u32(smem + L::DST + b * AT_TILE * BT * 2);
+        mbar_wait(p_full, it & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < BT / 16; ++kk)  // P^T of warpgroup kk/2 at S^T[b] + 32*(kk/2)
+          umma_f16_ts(tDV, tS0 + 64 * b + (kk >> 1) * 32 + (kk & 1) * 8, mndesc(sdo, kk, BT), id_kv,
+                      it > 0 || kk > 0);
+        mbar_wait(ds_full, it & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < BT / 16; ++kk)
+          umma_f16_ss(tDK, kdesc(sdst, kk, AT_TILE), mndesc(sq, kk, BT), id_kv, it > 0 || kk > 0);
+        umma_commit(&qdo_empty[st]);
+      }
+      umma_commit(acc_full);
+    }
+  } else {
+    // compute: thread = key row c; warpgroup g owns query columns [32g, 32g+32) of each tile
+    const int g = warp >> 2, quad = warp & 3;
+    const int c = quad * 32 + lane;
+    const int qoff = 32 * g;
+    const int ct = threadIdx.x;
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const int64_t row_base = static_cast<int64_t>(bh) * p.s;
+    const int kv_row = kt * AT_TILE + c;
+    for (int it = 0; it < n_it; ++it) {
+      const int b = it & 1;
+      const int q0 = (q_first + it) * BT;
+      float* s_lse = stat + b * 2 * BT;
+      float* s_del = s_lse + BT;
+      if (ct < 2 * BT) {
+        const int qi = ct & (BT - 1);
+        const int q = q0 + qi;
+        if (ct < BT) s_lse[qi] = q < p.s ? p.lse[row_base + q] * LOG2E : 0.f;
+        else s_del[qi] = q < p.s ? p.delta[row_base + q] : 0.f;
+      }
+      named_barrier_sync(1, 256);
+      mbar_wait(&sdp_full[b], (it >> 1) & 1);
+      tc_fence_after();
+      uint32_t rs[32], rd[32];
+      tmem_ld32(tS0 + 64 * b + lane_off + qoff, rs);
+      tmem_ld32(tDP0 + 64 * b + lane_off + qoff, rd);
+      tmem_wait_ld();
+      const bool need_mask = q0 < (kt + 1) * AT_TILE || q0 + BT > p.s;  // tile touches the diagonal / tail
+      uint32_t pk[16];
+      float ds[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int qi = qoff + j;
+        float pr = fast_exp2(fmaf(__uint_as_float(rs[j]), p.scale_log2, -s_lse[qi]));
+        if (need_mask && (q0 + qi < kv_row || q0 + qi >= p.s)) pr = 0.f;
+        ds[j] = pr * (__uint_as_float(rd[j]) - s_del[qi]);
+        rs[j] = __float_as_uint(pr);
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(__uint_as_float(rs[2 * j]), __uint_as_float(rs[2 * j + 1]));
+      tmem_st16(tS0 + 64 * b + lane_off + qoff, pk);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(p_full);
+      uint8_t* dst = smem + L::DST + b * AT_TILE * BT * 2;
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        *reinterpret_cast<uint4*>(dst + swz64(c, qoff + v * 8)) =
+            make_uint4(pack_bf16(ds[v * 8], ds[v * 8 + 1]), pack_bf16(ds[v * 8 + 2], ds[v * 8 + 3]),
+                       pack_bf16(ds[v * 8 + 4], ds[v * 8 + 5]), pack_bf16(ds[v * 8 + 6], ds[v * 8 + 7]));
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(ds_full);
+    }
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    const int64_t tok = static_cast<int64_t>(kv_row) * p.b + bi;
+    __nv_bfloat16* dk = p.dqkv + tok * p.ld_dqkv + p.h + head * D;
+    __nv_bfloat16* dv = p.dqkv + tok * p.ld_dqkv + 2 * p.h + head * D;
+#pragma unroll
+    for (int ch = 0; ch < D / 64; ++ch) {
+      const int col = g * (D / 2) + ch * 32;
+      uint32_t rk[32], rv[32];
+      tmem_ld32(tDK + lane_off + col, rk);
+      tmem_ld32(tDV + lane_off + col, rv);
+      tmem_wait_ld();
+      if (kv_row < p.s) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          float fk[8], fv[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            fk[i] = __uint_as_float(rk[v * 8 + i]) * p.scale;
+            fv[i] = __uint_as_float(rv[v * 8 + i]);
+          }
+          *reinterpret_cast<uint4*>(dk + col + v * 8) =
+              make_uint4(pack_bf16(fk[0], fk[1]), pack_bf16(fk[2], fk[3]), pack_bf16(fk[4], fk[5]), pack_bf16(fk[6], fk[7]));
+          *reinterpret_cast<uint4*>(dv + col + v * 8) =
+              make_uint4(pack_bf16(fv[0], fv[1]), pack_bf16(fv[2], fv[3]), pack_bf16(fv[4], fv[5]), pack_bf16(fv[6], fv[7]));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+template <int D>
+struct Q4Smem {
+  static constexpr int Q = 0;
+  static constexpr int DO = Q + Tile<D>::BYTES;
+  static constexpr int KV = DO + Tile<D>::BYTES;             // BT_STAGES x (K, V) [64 x D]
+  static constexpr int DS = KV + BT_STAGES * 2 * Half<D>::BYTES;  // 2 x [128 x 64]
+  static constexpr int BAR = DS + 2 * AT_TILE * BT * 2;
+  static constexpr int TOTAL = BAR + 256;
+};
+
+template <int D>
+__global__ void __launch_bounds__(BWD4_THREADS, 1)
+    attn_bwd_dq4_kernel(const __grid_constant__ CUtensorMap tm_qkv128, const __grid_constant__ CUtensorMap tm_qkv64,
+                        const __grid_constant__ CUtensorMap tm_do128, const AttnParams p) {
+  using L = Q4Smem<D>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if ((smem_u32(smem) & 1023) != 0) __trap();
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR);
+  uint64_t* q_full = bars;               // 1
+  uint64_t* kv_full = bars + 1;          // BT_STAGES
+  uint64_t* kv_empty = bars + 4;         // BT_STAGES
+  uint64_t* sdp_full = bars + 7;         // 2
+  uint64_t* ds_full = bars + 9;          // 256 arrivals
+  uint64_t* dq_done = bars + 10;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
+
+  const int warp = warp_id(), lane = lane_id();
+  const int nq = (p.s + AT_TILE - 1) / AT_TILE;
+  const int qt = nq - 1 - static_cast<int>(blockIdx.x);
+  const int q_last = min(p.s, (qt + 1) * AT_TILE) - 1;
+  const int nkv = q_last / BT + 1;  // 64-row key tiles 0 .. diag
+  const int bh = blockIdx.y;
+  const int bi = bh / p.heads, head = bh % p.heads;
+  const int qcol = head * D, kcol = p.h + head * D, vcol = 2 * p.h + head * D;
+
+  if (warp == 8 && lane == 0) {
+    tma_prefetch(&tm_qkv128);
+    tma_prefetch(&tm_qkv64);
+    tma_prefetch(&tm_do128);
+    for (int i = 0; i < 11; ++i) mbar_init(&bars[i], i == 9 ? 256 : 1);
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS0 = tmem, tDP0 = tmem + 128, tDQ = tmem + 256;
+
+  if (warp == 8) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(q_full, 2 * Tile<D>::BYTES);
+      tma_tile_rows<D>(smem + L::Q, &tm_qkv128, q_full, qcol, bi, qt * AT_TILE, AT_TILE);
+      tma_tile_rows<D>(smem + L::DO, &tm_do128, q_full, head * D, bi, qt * AT_TILE, AT_TILE);
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j % BT_STAGES;
+        mbar_wait(&kv_empty[st], ((j / BT_STAGES) & 1) ^ 1);
+        uint8_t* kb = smem + L::KV + st * 2 * Half<D>::BYTES;
+        mbar_arrive_expect_tx(&kv_full[st], 2 * Half<D>::BYTES);
+        tma_tile_rows<D>(kb, &tm_qkv64, &kv_full[st], kcol, bi, j * BT, BT);
+        tma_tile_rows<D>(kb + Half<D>::BYTES, &tm_qkv64, &kv_full[st], vcol, bi, j * BT, BT);
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {
+      constexpr uint32_t id_sp = idesc_bf16(128, BT, false, false);  // S, dP: M=128 q, N=64 kv
+      constexpr uint32_t id_q = idesc_bf16(128, D, false, true);     // dQ += dS K
+      const uint32_t sq = smem_u32(smem + L::Q), sdo = smem_u32(smem + L::DO);
+      auto skv = [&](int j) { return smem_u32(smem + L::KV + (j % BT_STAGES) * 2 * Half<D>::BYTES); };
+      auto issue_sdp = [&](int j) {
+        const int st = j % BT_STAGES, b = j & 1;
+        mbar_wait(&kv_full[st], (j / BT_STAGES) & 1);
+        tc_fence_after();
+        const uint32_t sk = skv(j), sv = sk + Half<D>::BYTES;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_f16_ss(tS0 + 64 * b, kdesc(sq, kk, AT_TILE), kdesc(sk, kk, BT), id_sp, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_f16_ss(tDP0 + 64 * b, kdesc(sdo, kk, AT_TILE), kdesc(sv, kk, BT), id_sp, kk > 0);
+        umma_commit(&sdp_full[b]);
+      };
+      mbar_wait(q_full, 0);
+      issue_sdp(0);
+      for (int j = 0; j < nkv; ++j) {
+        if (j + 1 < nkv) issue_sdp(j + 1);
+        mbar_wait(ds_full, j & 1);
+        tc_fence_after();
+        const uint32_t sds = smem_u32(smem + L::DS + (j & 1) * AT_TILE * BT * 2);
+#pragma unroll
+        for (int kk = 0; kk < BT / 16; ++kk)
+          umma_f16_ss(tDQ, kdesc(sds, kk, AT_TILE), mndesc(skv(j), kk, BT), id_q, j > 0 || kk > 0);
+        umma_commit(&kv_empty[j % BT_STAGES]);
+      }
+      umma_commit(dq_done);
+    }
+  } else {
+    // compute: thread = query row r; warpgroup g owns key columns [32g, 32g+32)
+    const int g = warp >> 2, quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const int koff = 32 * g;
+    const int q = qt * AT_TILE + r;
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const int64_t row = static_cast<int64_t>(bh) * p.s + q;
+    const float lse2 = q < p.s ? p.lse[row] * LOG2E : 0.f;
+    const float dlt = q < p.s ? p.delta[row] : 0.f;
+    for (int j = 0; j < nkv; ++j) {
+      const int b = j & 1;
+      mbar_wait(&sdp_full[b], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t rs[32], rd[32];
+      tmem_ld32(tS0 + 64 * b + lane_off + koff, rs);
+      tmem_ld32(tDP0 + 64 * b + lane_off + koff, rd);
+      tmem_wait_ld();
+      const int k0 = j * BT + koff;
+      const bool need_mask = k0 + 31 > qt * AT_TILE;  // some key index may exceed some query index
+      float ds[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        float pr = fast_exp2(fmaf(__uint_as_float(rs[i]), p.scale_log2, -lse2));
+        if (need_mask && k0 + i > q) pr = 0.f;
+        ds[i] = pr * (__uint_as_float(rd[i]) - dlt);
+      }
+      uint8_t* dss = smem + L::DS + b * AT_TILE * BT * 2;
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        *reinterpret_cast<uint4*>(dss + swz64(r, koff + v * 8)) =
+            make_uint4(pack_bf16(ds[v * 8], ds[v * 8 + 1]), pack_bf16(ds[v * 8 + 2], ds[v * 8 + 3]),
+                       pack_bf16(ds[v * 8 + 4], ds[v * 8 + 5]), pack_bf16(ds[v * 8 + 6], ds[v * 8 + 7]));
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(ds_full);
+    }
+    mbar_wait(dq_done, 0);
+    tc_fence_after();
+    __nv_bfloat16* dqp = p.dqkv + (static_cast<int64_t>(q) * p.b + bi) * p.ld_dqkv + head * D;
+#pragma unroll
+    for (int ch = 0; ch < D / 64; ++ch) {
+      const int col = g * (D / 2) + ch * 32;
+      uint32_t rq[32];
+      tmem_ld32(tDQ + lane_off + col, rq);
+      tmem_wait_ld();
+      if (q < p.s) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          float f[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(rq[v * 8 + i]) * p.scale;
+          *reinterpret_cast<uint4*>(dqp + col + v * 8) =
+              make_uint4(pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]), pack_bf16(f[6], f[7]));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// =====================================================================================
+// dQ kernel v5: every A operand in TMEM (smem traffic = one 64-row B tile per MMA)
+// =====================================================================================
+//
+// Q and dO are constant for the CTA: the compute warps copy them once into TMEM
+// in the packed A-operand layout (lane = query row, column c = K pair 2c,2c+1).
+// dS(j) goes from registers straight into TMEM over its own S columns.  All
+// three MMAs per 64-row key tile are then TS-form, reading only K_j / V_j from
+// shared memory: S = Q K_j^T, dP = dO V_j^T, dQ += dS K_j.
+// TMEM: S[b] 64b (dS at S[b] + 32g) | dP[b] 128+64b | dQ 256 | Q 384 | dO 384+D/2.
+
+template <int D>
+struct Q5Smem {
+  static constexpr int STAGES = 4;
+  static constexpr int KV = 0;  // STAGES x (K, V) [64 x D]
+  static constexpr int BAR = KV + STAGES * 2 * Half<D>::BYTES;
+  static constexpr int TOTAL = BAR + 256;
+};
+
+template <int D>
+__global__ void __launch_bounds__(BWD4_THREADS, 1)
+    attn_bwd_dq5_kernel(const __grid_constant__ CUtensorMap tm_qkv64, const __nv_bfloat16* __restrict__ qkv,
+                        int ld_qkv, const __nv_bfloat16* __restrict__ d_o, int ld_o, const AttnParams p) {
+  using L = Q5Smem<D>;
+  constexpr int ST = L::STAGES;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if ((smem_u32(smem) & 1023) != 0) __trap();
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR);
+  uint64_t* kv_full = bars;             // ST
+  uint64_t* kv_empty = bars + ST;       // ST
+  uint64_t* sdp_full = bars + 2 * ST;   // 2
+  uint64_t* ds_full = bars + 2 * ST + 2;  // 256 arrivals
+  uint64_t* qdo_ready = bars + 2 * ST + 3;  // 256 arrivals
+  uint64_t* dq_done = bars + 2 * ST + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * ST + 5);
+  constexpr int NBARS = 2 * ST + 5;
+
+  const int warp = warp_id(), lane = lane_id();
+  const int nq = (p.s + AT_TILE - 1) / AT_TILE;
+  const int qt = nq - 1 - static_cast<int>(blockIdx.x);
+  const int q_last = min(p.s, (qt + 1) * AT_TILE) - 1;
+  const int nkv = q_last / BT + 1;
+  const int bh = blockIdx.y;
+  const int bi = bh / p.heads, head = bh % p.heads;
+  const int kcol = p.h + head * D, vcol = 2 * p.h + head * D;
+
+  if (warp == 8 && lane == 0) {
+    tma_prefetch(&tm_qkv64);
+    for (int i = 0; i < NBARS; ++i)
+      mbar_init(&bars[i], (i == 2 * ST + 2 || i == 2 * ST + 3) ? 256 : 1);
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS0 = tmem, tDP0 = tmem + 128, tDQ = tmem + 256, tQ = tmem + 384, tDO = tmem + 384 + D / 2;
+
+  if (warp == 8) {
+    if (lane == 0) {
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j % ST;
+        mbar_wait(&kv_empty[st], ((j / ST) & 1) ^ 1);
+        uint8_t* kb = smem + L::KV + st * 2 * Half<D>::BYTES;
+        mbar_arrive_expect_tx(&kv_full[st], 2 * Half<D>::BYTES);
+        tma_tile_rows<D>(kb, &tm_qkv64, &kv_full[st], kcol, bi, j * BT, BT);
+        tma_tile_rows<D>(kb + Half<D>::BYTES, &tm_qkv64, &kv_full[st], vcol, bi, j * BT, BT);
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {
+      constexpr uint32_t id_sp = idesc_bf16(128, BT, false, false);
+      constexpr uint32_t id_q = idesc_bf16(128, D, false, true);
+      auto skv = [&](int j) { return smem_u32(smem + L::KV + (j % ST) * 2 * Half<D>::BYTES); };
+      auto issue_sdp = [&](int j) {
+        const int b = j & 1;
+        mbar_wait(&kv_full[j % ST], (j / ST) & 1);
+        tc_fence_after();
+        const uint32_t sk = skv(j), sv = sk + Half<D>::BYTES;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_f16_ts(tS0 + 64 * b, tQ + kk * 8, kdesc(sk, kk, BT), id_sp, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_f16_ts(tDP0 + 64 * b, tDO + kk * 8, kdesc(sv, kk, BT), id_sp, kk > 0);
+        umma_commit(&sdp_full[b]);
+      };
+      mbar_wait(qdo_ready, 0);
+      tc_fence_after();
+      issue_sdp(0);
+      for (int j = 0; j < nkv; ++j) {
+        if (j + 1 < nkv) issue_sdp(j + 1);
+        mbar_wait(ds_full, j & 1);
+        tc_fence_after();
+        const uint32_t tds = tS0 + 64 * (j & 1);
+#pragma unroll
+        for (int kk = 0; kk < BT / 16; ++kk)
+          umma_f16_ts(tDQ, tds + (kk >> 1) * 32 + (kk & 1) * 8, mndesc(skv(j), kk, BT), id_q, j > 0 || kk > 0);
+        umma_commit(&kv_empty[j % ST]);
+      }
+      umma_commit(dq_done);
+    }
+  } else {
+    const int g = warp >> 2, quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const int koff = 32 * g;
+    const int q = qt * AT_TILE + r;
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    {  // Q and dO rows -> TMEM (this warpgroup's half of the head dimension)
+      const int64_t tok = static_cast<int64_t>(q) * p.b + bi;
+      const uint4* qsrc = reinterpret_cast<const uint4*>(qkv + tok * ld_qkv + head * D + g * (D / 2));
+      const uint4* osrc = reinterpret_cast<const uint4*>(d_o + tok * ld_o + head * D + g * (D / 2));
+      // D/2 bf16 per warpgroup = D/16 uint4 = D/4 packed TMEM columns
+      if constexpr (D == 128) {
+        uint32_t wq[32], wo[32];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const uint4 a = q < p.s ? qsrc[v] : make_uint4(0, 0, 0, 0);
+          const uint4 o = q < p.s ? osrc[v] : make_uint4(0, 0, 0, 0);
+          wq[4 * v] = a.x; wq[4 * v + 1] = a.y; wq[4 * v + 2] = a.z; wq[4 * v + 3] = a.w;
+          wo[4 * v] = o.x; wo[4 * v + 1] = o.y; wo[4 * v + 2] = o.z; wo[4 * v + 3] = o.w;
+        }
+        tmem_st32(tQ + lane_off + g * 32, wq);
+        tmem_st32(tDO + lane_off + g * 32, wo);
+      } else {
+        uint32_t wq[16], wo[16];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const uint4 a = q < p.s ? qsrc[v] : make_uint4(0, 0, 0, 0);
+          const uint4 o = q < p.s ? osrc[v] : make_uint4(0, 0, 0, 0);
+          wq[4 * v] = a.x; wq[4 * v + 1] = a.y; wq[4 * v + 2] = a.z; wq[4 * v + 3] = a.w;
+          wo[4 * v] = o.x; wo[4 * v + 1] = o.y; wo[4 * v + 2] = o.z; wo[4 * v + 3] = o.w;
+        }
+        tmem_st16(tQ + lane_off + g * 16, wq);
+        tmem_st16(tDO + lane_off + g * 16, wo);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(qdo_ready);
+    }
+    const int64_t row = static_cast<int64_t>(bh) * p.s + q;
+    const float lse2 = q < p.s ? p.lse[row] * LOG2E : 0.f;
+    const float dlt = q < p.s ? p.delta[row] : 0.f;
+    for (int j = 0; j < nkv; ++j) {
+      const int b = j & 1;
+      mbar_wait(&sdp_full[b], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t rs[32], rd[32];
+      tmem_ld32(tS0 + 64 * b + lane_off + koff, rs);
+      tmem_ld32(tDP0 + 64 * b + lane_off + koff, rd);
+      tmem_wait_ld();
+      const int k0 = j * BT + koff;
+      const bool need_mask = k0 + 31 > qt * AT_TILE;
+      uint32_t pk[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        float p0 = fast_exp2(fmaf(__uint_as_float(rs[2 * i]), p.scale_log2, -lse2));
+        float p1 = fast_exp2(fmaf(__uint_as_float(rs[2 * i + 1]), p.scale_log2, -lse2));
+        if (need_mask && k0 + 2 * i > q) p0 = 0.f;
+        if (need_mask && k0 + 2 * i + 1 > q) p1 = 0.f;
+        pk[i] = pack_bf16(p0 * (__uint_as_float(rd[2 * i]) - dlt), p1 * (__uint_as_float(rd[2 * i + 1]) - dlt));
+      }
+      tmem_st16(tS0 + 64 * b + lane_off + koff, pk);  // dS over this warpgroup's own S columns
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(ds_full);
+    }
+    mbar_wait(dq_done, 0);
+    tc_fence_after();
+    __nv_bfloat16* dqp = p.dqkv + (static_cast<int64_t>(q) * p.b + bi) * p.ld_dqkv + head * D;
+#pragma unroll
+    for (int ch = 0; ch < D / 64; ++ch) {
+      const int col = g * (D / 2) + ch * 32;
+      uint32_t rq[32];
+      tmem_ld32(tDQ + lane_off + col, rq);
+      tmem_wait_ld();
+      if (q < p.s) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          float f[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(rq[v * 8 + i]) * p.scale;
+          *reinterpret_cast<uint4*>(dqp + col + v * 8) =
+              make_uint4(pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]), pack_bf16(f[6], f[7]));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 // D = rowsum(dO * O) per (batch, head, query); also zeroes the dQ accumulator.
 template <int D>
 __global__ void __launch_bounds__(256) attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ o,
@@ -1478,7 +2076,7 @@ static cudaError_t bwd_launch(const void* qkv, int ld_qkv, const void* o, const 
   if (e != cudaSuccess) return e;
   const int tokens = p.s * p.b;
   // HX_ATTN_BWD=1 / 2: the earlier single-kernel variants with dQ atomics (kept for A/B runs)
-  static const int variant = getenv("HX_ATTN_BWD") ? atoi(getenv("HX_ATTN_BWD")) : 3;
+  static const int variant = getenv("HX_ATTN_BWD") ? atoi(getenv("HX_ATTN_BWD")) : 4;
   static bool cfg = false;
   if (!cfg) {
     e = cudaFuncSetAttribute(attn_bwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdSmem<D>::TOTAL);
@@ -1488,15 +2086,37 @@ static cudaError_t bwd_launch(const void* qkv, int ld_qkv, const void* o, const 
       e = cudaFuncSetAttribute(attn_bwd_dkdv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, KVSmem<D>::TOTAL);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(attn_bwd_dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, QSmem<D>::TOTAL);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(attn_bwd_dkdv4_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, KV4Smem<D>::TOTAL);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(attn_bwd_dq4_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Q4Smem<D>::TOTAL);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(attn_bwd_dq5_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Q5Smem<D>::TOTAL);
     if (e != cudaSuccess) return e;
     cfg = true;
   }
-  const bool atomics = variant != 3;
+  const bool atomics = variant < 3;
   attn_bwd_pre_kernel<D><<<(tokens + 7) / 8, 256, 0, st>>>(
       static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(d_o), ld_o,
       const_cast<float*>(p.delta), atomics ? p.dq_acc : nullptr, p.s, p.b, p.heads);
   const int nq = (p.s + AT_TILE - 1) / AT_TILE;
   dim3 grid(nq, p.b * p.heads);
+  if (variant == 4) {
+    CUtensorMap tq64, tdo64;
+    e = make_tma_3d_rows(&tq64, qkv, 3 * p.h, p.b, p.s, ld_qkv, 64, BT);
+    if (e == cudaSuccess) e = make_tma_3d_rows(&tdo64, d_o, p.h, p.b, p.s, ld_o, 64, BT);
+    if (e != cudaSuccess) return e;
+    attn_bwd_dkdv4_kernel<D><<<grid, BWD4_THREADS, KV4Smem<D>::TOTAL, st>>>(tq, tq64, tdo64, p);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    static const bool dq4 = getenv("HX_ATTN_DQ4") != nullptr;
+    if (dq4)
+      attn_bwd_dq4_kernel<D><<<grid, BWD4_THREADS, Q4Smem<D>::TOTAL, st>>>(tq, tq64, tdo, p);
+    else
+      attn_bwd_dq5_kernel<D><<<grid, BWD4_THREADS, Q5Smem<D>::TOTAL, st>>>(
+          tq64, static_cast<const __nv_bfloat16*>(qkv), ld_qkv, static_cast<const __nv_bfloat16*>(d_o), ld_o, p);
+    return cudaGetLastError();
+  }
   if (!atomics) {
     attn_bwd_dkdv_kernel<D><<<grid, BWD3_THREADS, KVSmem<D>::TOTAL, st>>>(tq, tdo, p);
     e = cudaGetLastError();

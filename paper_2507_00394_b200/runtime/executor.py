@@ -448,10 +448,11 @@ def _multistream(core: _Core, timer: _Timer) -> None:
 # --- distributed -----------------------------------------------------------------------
 
 
-def _payload_layout(cfg, edge_tag: str, qkv: bool) -> list[tuple[str, tuple, torch.dtype]]:
+def _payload_layout(cfg, edge_tag: str, qkv: bool, math=None) -> list[tuple[str, tuple, torch.dtype]]:
     """Tensor names/shapes/dtypes of each edge's payload (``layers.py`` dict keys)."""
     T, h = cfg.s * cfg.b, cfg.h
-    bf, f32 = torch.bfloat16, torch.float32
+    bf = getattr(math, "act_dtype", torch.bfloat16)
+    f32 = getattr(math, "wgrad_dtype", torch.float32)
     act = lambda n, w=h: (n, (T, w), bf)  # noqa: E731
     if edge_tag == "pa":
         return [act("ln_out"), act("residual"), ("qkv_weight", (h, 3 * h), bf)] if qkv \
@@ -525,7 +526,7 @@ class _Distributed:
         while self.next_recv.get(src, 0) <= min(want + self.lookahead, len(seq) - 1):
             k = self.next_recv.get(src, 0)
             r_id = seq[k]
-            layout = _payload_layout(cfg, _edge_tag(r_id), core.qkv)
+            layout = _payload_layout(cfg, _edge_tag(r_id), core.qkv, core.math)
             st = core.stages[self.rank]
             payload, works = {}, []
             for name, shape, dtype in layout:
@@ -558,7 +559,7 @@ class _Distributed:
                 core.run_compute(t)
             for snd in core.sends_by_producer.get(tid, ()):
                 payload = core.checked_payload(snd)
-                layout = _payload_layout(core.cfg, _edge_tag(snd.id), core.qkv)
+                layout = _payload_layout(core.cfg, _edge_tag(snd.id), core.qkv, core.math)
                 grp = self.groups[(r, snd.peer)]
                 for name, _shape, dtype in layout:
                     tensor = payload[name].contiguous()
@@ -611,6 +612,7 @@ class HelixRuntime:
         local = [rank] if mode == "distributed" else list(range(sched.n_stages))
         self.stages = {si: _Stage(si, self.device, None) for si in local}
         self.sumsq = torch.zeros(self.cfg.m, dtype=torch.float64, device=self.device)
+        self.timeline = None
         self.core = _Core(sched, model, self.math, self.stages, self.sumsq)
         self.groups = groups
         self.record_timeline = record_timeline

@@ -34,7 +34,10 @@ def payload_elements(payload: Arrays) -> int:
 
 
 class LayerMath:
-    """Component kernels for one model shape; owns the attention workspaces."""
+    """Component kernels for one model shape (bf16 activations, fp32 grads)."""
+
+    act_dtype = torch.bfloat16     # activations / payload tensors / qkv_weight copies
+    wgrad_dtype = torch.float32    # shipped weight gradients (d_qkv_weight)
 
     def __init__(self, cfg, qkv_in_attention: bool, mlp_chunk: int | None, device):
         self.cfg = cfg

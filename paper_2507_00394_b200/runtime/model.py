@@ -100,10 +100,11 @@ class DeviceLayer:
     post lands on it, ``P/partition.py:25-36``).
     """
 
-    def __init__(self, tensors: dict[str, torch.Tensor], owned: tuple[str, ...]):
+    def __init__(self, tensors: dict[str, torch.Tensor], owned: tuple[str, ...],
+                 grad_dtype: torch.dtype = torch.float32):
         self.w = tensors
         self.grad: dict[str, torch.Tensor] = {
-            n: torch.zeros(tensors[n].shape, dtype=torch.float32, device=tensors[n].device)
+            n: torch.zeros(tensors[n].shape, dtype=grad_dtype, device=tensors[n].device)
             for n in owned}
 
     def __getitem__(self, name: str) -> torch.Tensor:

@@ -70,12 +70,13 @@ HX_API int hx_ln_fwd(const void* x, const float* gain, const float* bias, void* 
 
 /*
  * dx = LN_B(dy, x, gain) (+ dres if non-null); dgain_acc += sum_rows dy*xhat;
- * dbias_acc += sum_rows dy.  Stats are recomputed from x as the reference does.
+ * dbias_acc += sum_rows dy.  Stats are recomputed from x as the reference does
+ * and left in stats_ws (2*rows floats: mean, rstd per row).
  * Replaces mathops.layernorm_backward_b/_w (P/runtime/mathops.py:52-72) plus the
  * residual adds of layers.py:149 and :198.
  */
 HX_API int hx_ln_bwd(const void* dy, const void* x, const float* gain, const void* dres, void* dx,
-              float* dgain_acc, float* dbias_acc, int rows, int h, void* stream);
+              float* dgain_acc, float* dbias_acc, float* stats_ws, int rows, int h, void* stream);
 
 /*
  * Causal multi-head attention forward (flash, tcgen05).  qkv is [s*b, ld_qkv]

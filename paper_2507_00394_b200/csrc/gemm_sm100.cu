@@ -279,7 +279,10 @@ static int pick_bn(int M, int N, int num_sms) {
   };
   // 256-wide tiles halve A re-reads and smem traffic per FLOP; only give them up
   // for a clearly better wave quantisation.
-  return eff(t128, 1.0) > eff(t256, 1.0) + 0.12 ? 128 : 256;
+  // Measured on B200: 128-wide tiles run ~20% slower per FLOP (they need 96 B/clk
+  // of smem operand bandwidth vs 64 for 256-wide), so only a large wave-
+  // quantisation gain justifies them.
+  return eff(t128, 1.0) > eff(t256, 1.0) + 0.25 ? 128 : 256;
 }
 
 cudaError_t gemm_launch(const GemmOperand& a, const GemmOperand& b, const GemmParams& p,

@@ -114,11 +114,12 @@ int hx_ln_fwd(const void* x, const float* gain, const float* bias, void* y, int 
 }
 
 int hx_ln_bwd(const void* dy, const void* x, const float* gain, const void* dres, void* dx, float* dgain_acc,
-              float* dbias_acc, int rows, int h, void* stream) {
+              float* dbias_acc, float* stats_ws, int rows, int h, void* stream) {
   if (rows <= 0 || h <= 0 || h % 8 || h > 8192) return HX_E_SHAPE;
-  if (!aligned16(dy) || !aligned16(x) || !aligned16(dx) || !aligned16(gain) || (dres && !aligned16(dres)))
+  if (!aligned16(dy) || !aligned16(x) || !aligned16(dx) || !aligned16(gain) || (dres && !aligned16(dres)) ||
+      !aligned16(stats_ws))
     return HX_E_ALIGN;
-  return ret(ln_bwd_launch(dy, x, gain, dres, dx, dgain_acc, dbias_acc, rows, h, as_stream(stream)), 1);
+  return ret(ln_bwd_launch(dy, x, gain, dres, dx, dgain_acc, dbias_acc, stats_ws, rows, h, as_stream(stream)), 2);
 }
 
 int hx_attn_fwd(const void* qkv, int ld_qkv, void* o, int ld_o, float* lse, int s, int b, int heads, int d,

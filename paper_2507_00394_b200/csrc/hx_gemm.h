@@ -39,7 +39,7 @@ cudaError_t make_tma_3d_rows(CUtensorMap* map, const void* ptr, uint64_t cols, u
 cudaError_t ln_fwd_launch(const void* x, const float* g, const float* b, void* y, int rows, int h,
                           cudaStream_t st);
 cudaError_t ln_bwd_launch(const void* dy, const void* x, const float* g, const void* dres, void* dx,
-                          float* dg, float* db, int rows, int h, cudaStream_t st);
+                          float* dg, float* db, float* stats, int rows, int h, cudaStream_t st);
 cudaError_t mse_loss_launch(const void* z, int64_t n, void* dz, double* sumsq, cudaStream_t st);
 cudaError_t axpy_f32_launch(float* y, const float* x, int64_t n, cudaStream_t st);
 cudaError_t attn_fwd_launch(const void* qkv, int ld_qkv, void* o, int ld_o, float* lse, int s, int b,

@@ -74,115 +74,145 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16* __rest
   }
 }
 
-// Persistent: each warp walks rows; per-column dgain/dbias partials live in
-// shared memory and are flushed once per block with fp32 atomics.
+// LN backward, input-gradient half: one warp per row, row data in registers,
+// dx = rstd*(dy*g - mean(dy*g) - xhat*mean(dy*g*xhat)) (+ dres).  Also stores
+// the row's (mean, rstd) for the column-reduction kernel below.
 template <int NV>
-__global__ void __launch_bounds__(256) ln_bwd_kernel(
+__global__ void __launch_bounds__(256) ln_bwd_dx_kernel(
     const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
     const float* __restrict__ gain, const __nv_bfloat16* __restrict__ dres,
-    __nv_bfloat16* __restrict__ dx, float* __restrict__ dgain_acc, float* __restrict__ dbias_acc,
-    int rows, int h) {
-  extern __shared__ float red[];  // [2*h]: dgain, dbias partials
-  for (int i = threadIdx.x; i < 2 * h; i += blockDim.x) red[i] = 0.f;
-  __syncthreads();
+    __nv_bfloat16* __restrict__ dx, float2* __restrict__ stats, int rows, int h) {
+  const int row = blockIdx.x * 8 + warp_id();
+  if (row >= rows) return;
   const int lane = lane_id();
   const int nvec = h / 8;
-  const int warps_total = gridDim.x * 8;
-  for (int row = blockIdx.x * 8 + warp_id(); row < rows; row += warps_total) {
-    const int64_t off = static_cast<int64_t>(row) * h;
-    float xv[NV][8], gv[NV][8];
-    float sum = 0.f;
+  const int64_t off = static_cast<int64_t>(row) * h;
+  float xv[NV][8], gv[NV][8];
+  float sx = 0.f, sxx = 0.f;
 #pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      const int c = lane + 32 * i;
-      if (c < nvec) {
-        uint4 ux = reinterpret_cast<const uint4*>(x + off)[c];
-        uint4 ud = reinterpret_cast<const uint4*>(dy + off)[c];
-        const uint32_t wx[4] = {ux.x, ux.y, ux.z, ux.w};
-        const uint32_t wd[4] = {ud.x, ud.y, ud.z, ud.w};
+  for (int i = 0; i < NV; ++i) {
+    const int c = lane + 32 * i;
+    if (c < nvec) {
+      const uint4 ux = reinterpret_cast<const uint4*>(x + off)[c];
+      const uint4 ud = reinterpret_cast<const uint4*>(dy + off)[c];
+      const float4 g0 = reinterpret_cast<const float4*>(gain)[2 * c];
+      const float4 g1 = reinterpret_cast<const float4*>(gain)[2 * c + 1];
+      const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+      const uint32_t wx[4] = {ux.x, ux.y, ux.z, ux.w}, wd[4] = {ud.x, ud.y, ud.z, ud.w};
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          float2 fx = unpack_bf16(wx[j]);
-          float2 fd = unpack_bf16(wd[j]);
-          xv[i][2 * j] = fx.x;
-          xv[i][2 * j + 1] = fx.y;
-          gv[i][2 * j] = fd.x;  // dy for now
-          gv[i][2 * j + 1] = fd.y;
-          sum += fx.x + fx.y;
-        }
-      }
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    const float mu = sum / h;
-    float sq = 0.f;
-#pragma unroll
-    for (int i = 0; i < NV; ++i)
-      if (lane + 32 * i < nvec)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float d = xv[i][j] - mu;
-          sq += d * d;
-        }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-    const float inv = rsqrtf(sq / h + LN_EPS);
-    // xhat in xv, dxhat = dy * gain; reduce mean(dxhat), mean(dxhat * xhat)
-    float s1 = 0.f, s2 = 0.f;
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      const int c = lane + 32 * i;
-      if (c < nvec) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int col = 8 * c + j;
-          const float xh = (xv[i][j] - mu) * inv;
-          const float d = gv[i][j];
-          // transposed [8][h/8] layout: consecutive lanes hit consecutive banks
-          atomicAdd(&red[j * nvec + c], d * xh);
-          atomicAdd(&red[h + j * nvec + c], d);
-          const float dxh = d * gain[col];
-          xv[i][j] = xh;
-          gv[i][j] = dxh;
-          s1 += dxh;
-          s2 += dxh * xh;
-        }
-      }
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-    }
-    const float m1 = s1 / h, m2 = s2 / h;
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      const int c = lane + 32 * i;
-      if (c < nvec) {
-        float o[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) o[j] = inv * (gv[i][j] - m1 - xv[i][j] * m2);
-        if (dres) {
-          uint4 ur = reinterpret_cast<const uint4*>(dres + off)[c];
-          const uint32_t wr[4] = {ur.x, ur.y, ur.z, ur.w};
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            float2 f = unpack_bf16(wr[j]);
-            o[2 * j] += f.x;
-            o[2 * j + 1] += f.y;
-          }
-        }
-        reinterpret_cast<uint4*>(dx + off)[c] =
-            make_uint4(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]), pack_bf16(o[4], o[5]),
-                       pack_bf16(o[6], o[7]));
+      for (int j = 0; j < 4; ++j) {
+        const float2 fx = unpack_bf16(wx[j]), fd = unpack_bf16(wd[j]);
+        xv[i][2 * j] = fx.x;
+        xv[i][2 * j + 1] = fx.y;
+        gv[i][2 * j] = fd.x * gg[2 * j];  // dxhat = dy * gain
+        gv[i][2 * j + 1] = fd.y * gg[2 * j + 1];
+        sx += fx.x + fx.y;
       }
     }
   }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sx += __shfl_xor_sync(0xffffffffu, sx, o);
+  const float mu = sx / h;
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+    if (lane + 32 * i < nvec)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float d = xv[i][j] - mu;
+        sxx += d * d;
+      }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sxx += __shfl_xor_sync(0xffffffffu, sxx, o);
+  const float rstd = rsqrtf(sxx / h + LN_EPS);
+  float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+    if (lane + 32 * i < nvec)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        xv[i][j] = (xv[i][j] - mu) * rstd;
+        s1 += gv[i][j];
+        s2 += gv[i][j] * xv[i][j];
+      }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+  }
+  const float m1 = s1 / h, m2 = s2 / h;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = lane + 32 * i;
+    if (c < nvec) {
+      float o[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = rstd * (gv[i][j] - m1 - xv[i][j] * m2);
+      if (dres) {
+        const uint4 ur = reinterpret_cast<const uint4*>(dres + off)[c];
+        const uint32_t wr[4] = {ur.x, ur.y, ur.z, ur.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 f = unpack_bf16(wr[j]);
+          o[2 * j] += f.x;
+          o[2 * j + 1] += f.y;
+        }
+      }
+      reinterpret_cast<uint4*>(dx + off)[c] =
+          make_uint4(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]), pack_bf16(o[4], o[5]), pack_bf16(o[6], o[7]));
+    }
+  }
+  if (lane == 0) stats[row] = make_float2(mu, rstd);
+}
+
+// LN backward, weight half: dgain += sum_rows dy*xhat, dbias += sum_rows dy.
+// Block = 256 threads over 256 columns (8 per thread) x a chunk of rows; each
+// warp takes every 8th row, the 8 warps combine in smem, one fp32 atomic per
+// column per block.  Coalesced 512-byte row segments per warp.
+constexpr int LN_COL_ROWS = 256;
+__global__ void __launch_bounds__(256) ln_bwd_dgdb_kernel(const __nv_bfloat16* __restrict__ dy,
+                                                          const __nv_bfloat16* __restrict__ x,
+                                                          const float2* __restrict__ stats,
+                                                          float* __restrict__ dgain, float* __restrict__ dbias,
+                                                          int rows, int h) {
+  __shared__ float red[8][2][256 + 8];
+  const int lane = lane_id(), w = warp_id();
+  const int col = blockIdx.x * 256 + lane * 8;
+  const int r0 = blockIdx.y * LN_COL_ROWS;
+  const int r1 = min(rows, r0 + LN_COL_ROWS);
+  float ag[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ab[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (col < h) {
+    for (int r = r0 + w; r < r1; r += 8) {
+      const float2 st = stats[r];
+      const uint4 ux = *reinterpret_cast<const uint4*>(x + static_cast<int64_t>(r) * h + col);
+      const uint4 ud = *reinterpret_cast<const uint4*>(dy + static_cast<int64_t>(r) * h + col);
+      const uint32_t wx[4] = {ux.x, ux.y, ux.z, ux.w}, wd[4] = {ud.x, ud.y, ud.z, ud.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 fx = unpack_bf16(wx[j]), fd = unpack_bf16(wd[j]);
+        ag[2 * j] += fd.x * (fx.x - st.x) * st.y;
+        ag[2 * j + 1] += fd.y * (fx.y - st.x) * st.y;
+        ab[2 * j] += fd.x;
+        ab[2 * j + 1] += fd.y;
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    red[w][0][lane * 8 + j] = ag[j];
+    red[w][1][lane * 8 + j] = ab[j];
+  }
   __syncthreads();
-  for (int i = threadIdx.x; i < h; i += blockDim.x) {
-    const int t = (i & 7) * nvec + (i >> 3);
-    atomicAdd(&dgain_acc[i], red[t]);
-    atomicAdd(&dbias_acc[i], red[h + t]);
+  const int t = threadIdx.x;  // one column per thread
+  const int c = blockIdx.x * 256 + t;
+  if (c < h) {
+    float sg = 0.f, sb = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      sg += red[k][0][t];
+      sb += red[k][1][t];
+    }
+    atomicAdd(&dgain[c], sg);
+    atomicAdd(&dbias[c], sb);
   }
 }
 
@@ -256,21 +286,21 @@ cudaError_t ln_fwd_launch(const void* x, const float* g, const float* b, void* y
 }
 
 cudaError_t ln_bwd_launch(const void* dy, const void* x, const float* g, const void* dres, void* dx,
-                          float* dg, float* db, int rows, int h, cudaStream_t st) {
-  const int smem = 2 * h * static_cast<int>(sizeof(float));
-  int grid = num_sms() * 2;
-  if (grid * 8 > rows) grid = (rows + 7) / 8;
-#define L(NV)                                                                             \
-  do {                                                                                    \
-    auto k = ln_bwd_kernel<NV>;                                                           \
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
-    k<<<grid, 256, smem, st>>>(static_cast<const __nv_bfloat16*>(dy),                   \
-                               static_cast<const __nv_bfloat16*>(x), g,                  \
-                               static_cast<const __nv_bfloat16*>(dres),                  \
-                               static_cast<__nv_bfloat16*>(dx), dg, db, rows, h);        \
-  } while (0)
+                          float* dg, float* db, float* stats, int rows, int h, cudaStream_t st) {
+  const int grid = (rows + 7) / 8;
+  float2* st2 = reinterpret_cast<float2*>(stats);
+#define L(NV)                                                                                   \
+  ln_bwd_dx_kernel<NV><<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(dy),            \
+                                             static_cast<const __nv_bfloat16*>(x), g,           \
+                                             static_cast<const __nv_bfloat16*>(dres),           \
+                                             static_cast<__nv_bfloat16*>(dx), st2, rows, h)
   HX_NV_DISPATCH(h, L);
 #undef L
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  dim3 cg((h + 255) / 256, (rows + LN_COL_ROWS - 1) / LN_COL_ROWS);
+  ln_bwd_dgdb_kernel<<<cg, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(dy),
+                                         static_cast<const __nv_bfloat16*>(x), st2, dg, db, rows, h);
   return cudaGetLastError();
 }
 

@@ -27,7 +27,7 @@ SIGNATURES: dict[str, list] = {
     "hx_launch_count": [],
     "hx_gemm": [_P, _I, _I, _P, _I, _I, _P, _I, _I, _I, _I, _I, _P, _I, _P, _I, _P],
     "hx_ln_fwd": [_P, _P, _P, _P, _I, _I, _P],
-    "hx_ln_bwd": [_P, _P, _P, _P, _P, _P, _P, _I, _I, _P],
+    "hx_ln_bwd": [_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P],
     "hx_attn_fwd": [_P, _I, _P, _I, _P, _I, _I, _I, _I, _P],
     "hx_attn_bwd": [_P, _I, _P, _P, _I, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P],
     "hx_mse_loss": [_P, _LL, _P, _P, _P],

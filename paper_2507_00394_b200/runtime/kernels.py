@@ -120,9 +120,10 @@ def layernorm(x, gain, bias, out=None):
 
 def layernorm_bwd(dy, x, gain, dres, dx, dgain_acc, dbias_acc):
     dy, x = _rows(dy), _rows(x)
+    stats = torch.empty(2 * x.shape[0], dtype=F32, device=x.device)
     _lib.call("hx_ln_bwd", dy.data_ptr(), x.data_ptr(), gain.data_ptr(),
               _ptr(None if dres is None else _rows(dres)), dx.data_ptr(), dgain_acc.data_ptr(),
-              dbias_acc.data_ptr(), x.shape[0], x.shape[1], _stream())
+              dbias_acc.data_ptr(), stats.data_ptr(), x.shape[0], x.shape[1], _stream())
     return dx
 
 

@@ -1,0 +1,110 @@
+// Shared pieces of the causal flash-attention kernels (forward / backward).
+//
+// Tile layouts: a [rows x D] bf16 tile of one head is D/64 swizzle atoms of
+// [rows x 64] (rows*128 bytes each), written by TMA with SWIZZLE_128B.  The same
+// physical tile is a K-major UMMA operand (K = the 64-column atoms) or an
+// MN-major one (K = rows), so no transposed copies exist anywhere.
+// TMEM A operands ("packed"): lane = row, 32-bit column c holds K elements
+// (2c, 2c+1) as bf16x2.
+#pragma once
+
+#include "hx_common.cuh"
+#include "hx_gemm.h"
+
+namespace hx {
+
+constexpr int AT_TILE = 128;  // rows of a resident (M-side) tile
+constexpr int BT = 64;        // rows of a streamed tile in the backward kernels
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr float LN2 = 0.6931471805599453f;
+
+template <int D>
+struct Tile {  // [128 x D]
+  static constexpr int BYTES = AT_TILE * D * 2;
+};
+template <int D>
+struct Half {  // [64 x D]
+  static constexpr int BYTES = BT * D * 2;
+};
+
+struct AttnParams {
+  int s, b, heads, h;
+  float scale_log2;  // log2(e) / sqrt(d)
+  float scale;       // 1 / sqrt(d)
+  __nv_bfloat16* o;  // forward output [s*b, ld_o]
+  int ld_o;
+  float* lse;          // [b, heads, s], natural log
+  const float* delta;  // [b, heads, s], rowsum(dO * O)
+  __nv_bfloat16* dqkv;
+  int ld_dqkv;
+};
+
+// Smem descriptors for K-step kk (16 elements) of a tile with `rows` rows.
+HX_DEVICE uint64_t kdesc(uint32_t base, int kk, int rows) {  // K along the 64-col atoms
+  return sw128_desc(base + (kk >> 2) * rows * 128 + (kk & 3) * 32, 16, 1024);
+}
+HX_DEVICE uint64_t mndesc(uint32_t base, int kk, int rows) {  // K along rows, N/M along atoms
+  return sw128_desc(base + kk * 2048, rows * 128, 1024);
+}
+
+// [rows x D] tile of head columns col0.. for tokens s0.. of batch bi (3-D map {cols, b, s}).
+template <int D>
+HX_DEVICE void tma_tile_rows(void* dst, const CUtensorMap* map, uint64_t* bar, int col0, int bi, int s0,
+                             int rows) {
+#pragma unroll
+  for (int a = 0; a < D / 64; ++a)
+    tma_load_3d(static_cast<uint8_t*>(dst) + a * rows * 128, map, bar, col0 + 64 * a, bi, s0);
+}
+
+HX_DEVICE float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+HX_DEVICE void named_barrier_sync(uint32_t id, uint32_t threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+HX_DEVICE uint4 bf16x8(const float* f) {
+  return make_uint4(pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]), pack_bf16(f[6], f[7]));
+}
+
+// Copy NB bf16 values of one global row into packed TMEM columns (NB/2 of them).
+template <int NB>
+HX_DEVICE void row_to_tmem(uint32_t taddr, const __nv_bfloat16* src, bool valid) {
+  static_assert(NB == 16 || NB == 32 || NB == 64, "row chunk");
+  uint32_t w[NB / 2];
+#pragma unroll
+  for (int v = 0; v < NB / 8; ++v) {
+    const uint4 a = valid ? reinterpret_cast<const uint4*>(src)[v] : make_uint4(0, 0, 0, 0);
+    w[4 * v] = a.x; w[4 * v + 1] = a.y; w[4 * v + 2] = a.z; w[4 * v + 3] = a.w;
+  }
+  if constexpr (NB == 64) {
+    tmem_st32(taddr, w);
+  } else if constexpr (NB == 32) {
+    tmem_st16(taddr, w);
+  } else {
+    tmem_st8(taddr, w);
+  }
+}
+
+// Read NC fp32 accumulator columns of this thread's row, scale, store bf16 to global.
+template <int NC>
+HX_DEVICE void tmem_row_to_global(uint32_t taddr, __nv_bfloat16* dst, float scale, bool valid) {
+  static_assert(NC == 16 || NC == 32, "row chunk");
+  uint32_t r[NC];
+  if constexpr (NC == 32) tmem_ld32(taddr, r);
+  else tmem_ld16(taddr, r);
+  tmem_wait_ld();
+  if (!valid) return;
+#pragma unroll
+  for (int v = 0; v < NC / 8; ++v) {
+    float f[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(r[v * 8 + i]) * scale;
+    reinterpret_cast<uint4*>(dst)[v] = bf16x8(f);
+  }
+}
+
+}  // namespace hx

@@ -413,6 +413,369 @@ __global__ void __launch_bounds__((4 * NWG + 2) * 32, 1)
   }
 }
 
+// =====================================================================================
+// v9: 128-wide streamed tiles (every MMA at N >= 128, the full-rate shapes on B200:
+// a measured 64 cycles per 128x128x16 MMA, vs 45-48 for 128x64x16 instead of 32)
+// =====================================================================================
+//
+// dK/dV: CTA = 128-row key tile; streams 128-row query tiles.
+//   S^T(i) = K Q^T  SS -> 256 | dP^T(i) = V dO^T  SS -> 384 |
+//   [P^T packed over S^T] dV += P^T dO  TS | [dS^T packed over dP^T] dK += dS^T Q  TS
+//   The softmax of tile i overlaps dP^T(i); dS^T overlaps dV.
+//   TMEM: dK 0 | dV 128 | S^T 256 | dP^T 384.   smem: K, V + Q/dO x 2 stages.
+// dQ: CTA = 128-row query tile; streams 128-row key tiles.
+//   S(j) = Q K^T TS -> 0 | dP(j) = dO V^T TS -> 128 | [dS packed over dP] dQ += dS K TS
+//   S(j+1) is issued as soon as the softmax has read S(j), so it runs under dS(j).
+//   TMEM: S 0 | dP 128 | dQ 256 | Q 384 | dO 384+D/2.   smem: K/V x 3 stages.
+
+template <int D>
+struct KV9Smem {
+  static constexpr int STAGES = 2;
+  static constexpr int K = 0;
+  static constexpr int V = K + Tile<D>::BYTES;
+  static constexpr int Q = V + Tile<D>::BYTES;              // STAGES x [128 x D]
+  static constexpr int DO = Q + STAGES * Tile<D>::BYTES;    // STAGES x [128 x D]
+  static constexpr int STAT = DO + STAGES * Tile<D>::BYTES;  // [2][lse2 | delta][128]
+  static constexpr int BAR = STAT + 2 * 2 * AT_TILE * 4;
+  static constexpr int TOTAL = BAR + 256;
+};
+
+template <int D>
+__global__ void __launch_bounds__(320, 1)
+    attn_bwd_dkdv9_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                          const AttnParams p) {
+  using L = KV9Smem<D>;
+  constexpr int ST = L::STAGES;
+  constexpr int NT = 256;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if ((smem_u32(smem) & 1023) != 0) __trap();
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR);
+  uint64_t* qdo_full = bars;              // ST
+  uint64_t* qdo_empty = bars + ST;        // ST
+  uint64_t* kv_full = bars + 2 * ST;
+  uint64_t* s_full = bars + 2 * ST + 1;
+  uint64_t* dp_full = bars + 2 * ST + 2;
+  uint64_t* p_full = bars + 2 * ST + 3;   // NT arrivals
+  uint64_t* ds_full = bars + 2 * ST + 4;  // NT arrivals
+  uint64_t* acc_full = bars + 2 * ST + 5;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * ST + 6);
+  constexpr int NBARS = 2 * ST + 6;
+  float* stat = reinterpret_cast<float*>(smem + L::STAT);
+
+  const int warp = warp_id(), lane = lane_id();
+  const int nq = (p.s + AT_TILE - 1) / AT_TILE;
+  const int kt = static_cast<int>(blockIdx.x);  // heaviest key tiles first
+  const int bh = blockIdx.y;
+  const int bi = bh / p.heads, head = bh % p.heads;
+  const int qcol = head * D, kcol = p.h + head * D, vcol = 2 * p.h + head * D;
+  const int n_it = nq - kt;
+
+  if (warp == 8 && lane == 0) {
+    tma_prefetch(&tm_qkv);
+    tma_prefetch(&tm_do);
+    for (int i = 0; i < NBARS; ++i) mbar_init(&bars[i], (i == 2 * ST + 3 || i == 2 * ST + 4) ? NT : 1);
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tDK = tmem, tDV = tmem + 128, tS = tmem + 256, tDP = tmem + 384;
+
+  if (warp == 8) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(kv_full, 2 * Tile<D>::BYTES);
+      tma_tile_rows<D>(smem + L::K, &tm_qkv, kv_full, kcol, bi, kt * AT_TILE, AT_TILE);
+      tma_tile_rows<D>(smem + L::V, &tm_qkv, kv_full, vcol, bi, kt * AT_TILE, AT_TILE);
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it % ST, q0 = (kt + it) * AT_TILE;
+        mbar_wait(&qdo_empty[st], ((it / ST) & 1) ^ 1);
+        mbar_arrive_expect_tx(&qdo_full[st], 2 * Tile<D>::BYTES);
+        tma_tile_rows<D>(smem + L::Q + st * Tile<D>::BYTES, &tm_qkv, &qdo_full[st], qcol, bi, q0, AT_TILE);
+        tma_tile_rows<D>(smem + L::DO + st * Tile<D>::BYTES, &tm_do, &qdo_full[st], head * D, bi, q0, AT_TILE);
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {
+      constexpr uint32_t id_sp = idesc_bf16(128, 128, false, false);
+      constexpr uint32_t id_kv = idesc_bf16(128, D, false, true);
+      const uint32_t sk = smem_u32(smem + L::K), sv = smem_u32(smem + L::V);
+      mbar_wait(kv_full, 0);
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it % ST;
+        const uint32_t sq = smem_u32(smem + L::Q + st * Tile<D>::BYTES);
+        const uint32_t sdo = smem_u32(smem + L::DO + st * Tile<D>::BYTES);
+        mbar_wait(&qdo_full[st], (it / ST) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_f16_ss(tS, kdesc(sk, kk, AT_TILE), kdesc(sq, kk, AT_TILE), id_sp, kk > 0);
+        umma_commit(s_full);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_f16_ss(tDP, kdesc(sv, kk, AT_TILE), kdesc(sdo, kk, AT_TILE), id_sp, kk > 0);
+        umma_commit(dp_full);
+        mbar_wait(p_full, it & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < AT_TILE / 16; ++kk)
+          umma_f16_ts(tDV, packed_kstep<64>(tS, kk), mndesc(sdo, kk, AT_TILE), id_kv, it > 0 || kk > 0);
+        mbar_wait(ds_full, it & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < AT_TILE / 16; ++kk)
+          umma_f16_ts(tDK, packed_kstep<64>(tDP, kk), mndesc(sq, kk, AT_TILE), id_kv, it > 0 || kk > 0);
+        umma_commit(&qdo_empty[st]);
+      }
+      umma_commit(acc_full);
+    }
+  } else {
+    // compute: thread = key row c, query columns [64g, 64g + 64)
+    const int g = warp >> 2, quad = warp & 3;
+    const int c = quad * 32 + lane;
+    const int qoff = 64 * g;
+    const int ct = threadIdx.x;
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const int64_t row_base = static_cast<int64_t>(bh) * p.s;
+    const int kv_row = kt * AT_TILE + c;
+    float nxt = 0.f;
+    auto fetch = [&](int it) {  // thread ct < 128: lse2 of query ct, else delta of query ct-128
+      const int qi = ct & (AT_TILE - 1), q = (kt + it) * AT_TILE + qi;
+      nxt = q >= p.s ? 0.f : (ct < AT_TILE ? p.lse[row_base + q] * LOG2E : p.delta[row_base + q]);
+    };
+    fetch(0);
+    for (int it = 0; it < n_it; ++it) {
+      const int q0 = (kt + it) * AT_TILE;
+      float* s_lse = stat + (it & 1) * 2 * AT_TILE;
+      float* s_del = s_lse + AT_TILE;
+      (ct < AT_TILE ? s_lse : s_del)[ct & (AT_TILE - 1)] = nxt;
+      named_barrier_sync(1, NT);
+      if (it + 1 < n_it) fetch(it + 1);
+      const bool need_mask = it == 0 || q0 + AT_TILE > p.s;
+      mbar_wait(s_full, it & 1);
+      tc_fence_after();
+      uint32_t raw[64];
+      tmem_ld32(tS + lane_off + qoff, *reinterpret_cast<uint32_t(*)[32]>(raw));
+      tmem_ld32(tS + lane_off + qoff + 32, *reinterpret_cast<uint32_t(*)[32]>(raw + 32));
+      tmem_wait_ld();
+      float pv[64];
+#pragma unroll
+      for (int v = 0; v < 16; ++v) {
+        const float4 l4 = reinterpret_cast<const float4*>(s_lse + qoff)[v];
+        pv[4 * v] = fast_exp2(fmaf(__uint_as_float(raw[4 * v]), p.scale_log2, -l4.x));
+        pv[4 * v + 1] = fast_exp2(fmaf(__uint_as_float(raw[4 * v + 1]), p.scale_log2, -l4.y));
+        pv[4 * v + 2] = fast_exp2(fmaf(__uint_as_float(raw[4 * v + 2]), p.scale_log2, -l4.z));
+        pv[4 * v + 3] = fast_exp2(fmaf(__uint_as_float(raw[4 * v + 3]), p.scale_log2, -l4.w));
+      }
+      if (need_mask) {  // diagonal tile (query < key) and the sequence tail
+#pragma unroll
+        for (int j = 0; j < 64; ++j)
+          if (q0 + qoff + j < kv_row || q0 + qoff + j >= p.s) pv[j] = 0.f;
+      }
+      {
+        uint32_t pk[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) pk[j] = pack_bf16(pv[2 * j], pv[2 * j + 1]);
+        tmem_st32(tS + lane_off + qoff, pk);  // P^T over this warpgroup's S^T columns
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(p_full);
+      mbar_wait(dp_full, it & 1);
+      tc_fence_after();
+      tmem_ld32(tDP + lane_off + qoff, *reinterpret_cast<uint32_t(*)[32]>(raw));
+      tmem_ld32(tDP + lane_off + qoff + 32, *reinterpret_cast<uint32_t(*)[32]>(raw + 32));
+      tmem_wait_ld();
+      {
+        uint32_t pk[32];
+#pragma unroll
+        for (int v = 0; v < 16; ++v) {
+          const float4 d4 = reinterpret_cast<const float4*>(s_del + qoff)[v];
+          pk[2 * v] = pack_bf16(pv[4 * v] * (__uint_as_float(raw[4 * v]) - d4.x),
+                                pv[4 * v + 1] * (__uint_as_float(raw[4 * v + 1]) - d4.y));
+          pk[2 * v + 1] = pack_bf16(pv[4 * v + 2] * (__uint_as_float(raw[4 * v + 2]) - d4.z),
+                                    pv[4 * v + 3] * (__uint_as_float(raw[4 * v + 3]) - d4.w));
+        }
+        tmem_st32(tDP + lane_off + qoff, pk);  // dS^T over this warpgroup's dP^T columns
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(ds_full);
+    }
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    const int64_t kv_tok = static_cast<int64_t>(kv_row) * p.b + bi;
+    __nv_bfloat16* dst = p.dqkv + kv_tok * p.ld_dqkv + head * D;
+    acc_row_out<D, 2>(tDK + lane_off, g, dst + p.h, p.scale, kv_row < p.s);
+    acc_row_out<D, 2>(tDV + lane_off, g, dst + 2 * p.h, 1.f, kv_row < p.s);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+template <int D>
+struct Q9Smem {
+  static constexpr int STAGES = 3;
+  static constexpr int KV = 0;  // STAGES x (K, V) [128 x D]
+  static constexpr int BAR = KV + STAGES * 2 * Tile<D>::BYTES;
+  static constexpr int TOTAL = BAR + 256;
+};
+
+template <int D>
+__global__ void __launch_bounds__(320, 1)
+    attn_bwd_dq9_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __nv_bfloat16* __restrict__ qkv, int ld_qkv,
+                        const __nv_bfloat16* __restrict__ d_o, int ld_o, const AttnParams p) {
+  using L = Q9Smem<D>;
+  constexpr int ST = L::STAGES;
+  constexpr int NT = 256;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if ((smem_u32(smem) & 1023) != 0) __trap();
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR);
+  uint64_t* kv_full = bars;                 // ST
+  uint64_t* kv_empty = bars + ST;           // ST
+  uint64_t* s_full = bars + 2 * ST;
+  uint64_t* s_free = bars + 2 * ST + 1;     // NT arrivals
+  uint64_t* dp_full = bars + 2 * ST + 2;
+  uint64_t* ds_full = bars + 2 * ST + 3;    // NT arrivals
+  uint64_t* qdo_ready = bars + 2 * ST + 4;  // NT arrivals
+  uint64_t* dq_done = bars + 2 * ST + 5;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * ST + 6);
+  constexpr int NBARS = 2 * ST + 6;
+
+  const int warp = warp_id(), lane = lane_id();
+  const int nq = (p.s + AT_TILE - 1) / AT_TILE;
+  const int qt = nq - 1 - static_cast<int>(blockIdx.x);  // heaviest query tiles first
+  const int nkv = qt + 1;
+  const int bh = blockIdx.y;
+  const int bi = bh / p.heads, head = bh % p.heads;
+  const int kcol = p.h + head * D, vcol = 2 * p.h + head * D;
+
+  if (warp == 8 && lane == 0) {
+    tma_prefetch(&tm_qkv);
+    for (int i = 0; i < NBARS; ++i)
+      mbar_init(&bars[i], (i == 2 * ST + 1 || i == 2 * ST + 3 || i == 2 * ST + 4) ? NT : 1);
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem, tDP = tmem + 128, tDQ = tmem + 256, tQ = tmem + 384, tDO = tmem + 384 + D / 2;
+
+  if (warp == 8) {
+    if (lane == 0) {
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j % ST;
+        mbar_wait(&kv_empty[st], ((j / ST) & 1) ^ 1);
+        uint8_t* kb = smem + L::KV + st * 2 * Tile<D>::BYTES;
+        mbar_arrive_expect_tx(&kv_full[st], 2 * Tile<D>::BYTES);
+        tma_tile_rows<D>(kb, &tm_qkv, &kv_full[st], kcol, bi, j * AT_TILE, AT_TILE);
+        tma_tile_rows<D>(kb + Tile<D>::BYTES, &tm_qkv, &kv_full[st], vcol, bi, j * AT_TILE, AT_TILE);
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {
+      constexpr uint32_t id_sp = idesc_bf16(128, 128, false, false);
+      constexpr uint32_t id_q = idesc_bf16(128, D, false, true);
+      auto skv = [&](int j) { return smem_u32(smem + L::KV + (j % ST) * 2 * Tile<D>::BYTES); };
+      auto issue_s = [&](int j) {
+        mbar_wait(&kv_full[j % ST], (j / ST) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) umma_f16_ts(tS, tQ + kk * 8, kdesc(skv(j), kk, AT_TILE), id_sp, kk > 0);
+        umma_commit(s_full);
+      };
+      auto issue_dp = [&](int j) {
+        const uint32_t sv = skv(j) + Tile<D>::BYTES;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) umma_f16_ts(tDP, tDO + kk * 8, kdesc(sv, kk, AT_TILE), id_sp, kk > 0);
+        umma_commit(dp_full);
+      };
+      mbar_wait(qdo_ready, 0);
+      tc_fence_after();
+      issue_s(0);
+      issue_dp(0);
+      for (int j = 0; j < nkv; ++j) {
+        if (j + 1 < nkv) {
+          mbar_wait(s_free, j & 1);  // the softmax has read S(j)
+          issue_s(j + 1);
+        }
+        mbar_wait(ds_full, j & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < AT_TILE / 16; ++kk)
+          umma_f16_ts(tDQ, packed_kstep<64>(tDP, kk), mndesc(skv(j), kk, AT_TILE), id_q, j > 0 || kk > 0);
+        umma_commit(&kv_empty[j % ST]);
+        if (j + 1 < nkv) issue_dp(j + 1);
+      }
+      umma_commit(dq_done);
+    }
+  } else {
+    // compute: thread = query row r, key columns [64g, 64g + 64)
+    const int g = warp >> 2, quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const int koff = 64 * g;
+    const int q = qt * AT_TILE + r;
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const int64_t tok = static_cast<int64_t>(q) * p.b + bi;
+    row_to_tmem<D / 2>(tQ + lane_off + g * (D / 4), qkv + tok * ld_qkv + head * D + g * (D / 2), q < p.s);
+    row_to_tmem<D / 2>(tDO + lane_off + g * (D / 4), d_o + tok * ld_o + head * D + g * (D / 2), q < p.s);
+    tmem_wait_st();
+    tc_fence_before();
+    mbar_arrive(qdo_ready);
+    const int64_t row = static_cast<int64_t>(bh) * p.s + q;
+    const float lse2 = q < p.s ? p.lse[row] * LOG2E : 0.f;
+    const float dlt = q < p.s ? p.delta[row] : 0.f;
+    for (int j = 0; j < nkv; ++j) {
+      mbar_wait(s_full, j & 1);
+      tc_fence_after();
+      uint32_t raw[64];
+      tmem_ld32(tS + lane_off + koff, *reinterpret_cast<uint32_t(*)[32]>(raw));
+      tmem_ld32(tS + lane_off + koff + 32, *reinterpret_cast<uint32_t(*)[32]>(raw + 32));
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(s_free);
+      float pv[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i) pv[i] = fast_exp2(fmaf(__uint_as_float(raw[i]), p.scale_log2, -lse2));
+      if (j == qt) {  // diagonal tile
+#pragma unroll
+        for (int i = 0; i < 64; ++i)
+          if (koff + i > r) pv[i] = 0.f;
+      }
+      mbar_wait(dp_full, j & 1);
+      tc_fence_after();
+      tmem_ld32(tDP + lane_off + koff, *reinterpret_cast<uint32_t(*)[32]>(raw));
+      tmem_ld32(tDP + lane_off + koff + 32, *reinterpret_cast<uint32_t(*)[32]>(raw + 32));
+      tmem_wait_ld();
+      uint32_t pk[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        pk[i] = pack_bf16(pv[2 * i] * (__uint_as_float(raw[2 * i]) - dlt),
+                          pv[2 * i + 1] * (__uint_as_float(raw[2 * i + 1]) - dlt));
+      tmem_st32(tDP + lane_off + koff, pk);  // dS over this warpgroup's dP columns
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(ds_full);
+    }
+    mbar_wait(dq_done, 0);
+    tc_fence_after();
+    acc_row_out<D, 2>(tDQ + lane_off, g, p.dqkv + tok * p.ld_dqkv + head * D, p.scale, q < p.s);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 // ------------------------------------------------------------------ pre-pass
 
 // D = rowsum(dO * O) per (batch, head, query): one warp per token.
@@ -481,6 +844,35 @@ static cudaError_t bwd_launch(const void* qkv, int ld_qkv, const void* o, const 
   return cudaGetLastError();
 }
 
+template <int D>
+static cudaError_t bwd9_launch(const void* qkv, int ld_qkv, const void* o, const void* d_o, int ld_o,
+                               const AttnParams& p, cudaStream_t st) {
+  CUtensorMap tq, tdo;
+  cudaError_t e = make_tma_3d_rows(&tq, qkv, 3 * p.h, p.b, p.s, ld_qkv, 64, AT_TILE);
+  if (e == cudaSuccess) e = make_tma_3d_rows(&tdo, d_o, p.h, p.b, p.s, ld_o, 64, AT_TILE);
+  if (e != cudaSuccess) return e;
+  static bool cfg = false;
+  if (!cfg) {
+    e = cudaFuncSetAttribute(attn_bwd_dkdv9_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             KV9Smem<D>::TOTAL);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(attn_bwd_dq9_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Q9Smem<D>::TOTAL);
+    if (e != cudaSuccess) return e;
+    cfg = true;
+  }
+  const int tokens = p.s * p.b;
+  attn_bwd_pre_kernel<D><<<(tokens + 7) / 8, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(o),
+                                                           static_cast<const __nv_bfloat16*>(d_o), ld_o,
+                                                           const_cast<float*>(p.delta), p.s, p.b, p.heads);
+  dim3 grid((p.s + AT_TILE - 1) / AT_TILE, p.b * p.heads);
+  attn_bwd_dkdv9_kernel<D><<<grid, 320, KV9Smem<D>::TOTAL, st>>>(tq, tdo, p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  attn_bwd_dq9_kernel<D><<<grid, 320, Q9Smem<D>::TOTAL, st>>>(tq, static_cast<const __nv_bfloat16*>(qkv), ld_qkv,
+                                                               static_cast<const __nv_bfloat16*>(d_o), ld_o, p);
+  return cudaGetLastError();
+}
+
 cudaError_t attn_bwd_launch(const void* qkv, int ld_qkv, const void* o, const void* d_o, int ld_o,
                             const float* lse, float* delta, float* /*dq_ws: unused, atomic-free*/, void* dqkv,
                             int ld_dqkv, int s, int b, int heads, int d, cudaStream_t st) {
@@ -495,7 +887,14 @@ cudaError_t attn_bwd_launch(const void* qkv, int ld_qkv, const void* o, const vo
   p.delta = delta;
   p.dqkv = static_cast<__nv_bfloat16*>(dqkv);
   p.ld_dqkv = ld_dqkv;
-  // HX_ATTN_NWG=4 selects four compute warpgroups (A/B runs); default two.
+  // Default: the 128-wide v9 kernels.  HX_ATTN_BWD=8 selects the 64-wide kernels
+  // (HX_ATTN_NWG=2|4 compute warpgroups) for A/B runs.
+  static const int variant = getenv("HX_ATTN_BWD") ? atoi(getenv("HX_ATTN_BWD")) : 9;
+  if (variant == 9) {
+    if (d == 128) return bwd9_launch<128>(qkv, ld_qkv, o, d_o, ld_o, p, st);
+    if (d == 64) return bwd9_launch<64>(qkv, ld_qkv, o, d_o, ld_o, p, st);
+    return cudaErrorNotSupported;
+  }
   static const int nwg = getenv("HX_ATTN_NWG") ? atoi(getenv("HX_ATTN_NWG")) : 2;
   if (d == 128) return nwg == 2 ? bwd_launch<128, 2>(qkv, ld_qkv, o, d_o, ld_o, p, st)
                                 : bwd_launch<128, 4>(qkv, ld_qkv, o, d_o, ld_o, p, st);

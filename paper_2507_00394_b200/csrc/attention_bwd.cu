@@ -563,10 +563,10 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
       for (int v = 0; v < 16; ++v) {
         const float4 l4 = reinterpret_cast<const float4*>(s_lse + qoff)[v];
-        pv[4 * v] = fast_exp2(fmaf(__uint_as_float(raw[4 * v]), p.scale_log2, -l4.x));
-        pv[4 * v + 1] = fast_exp2(fmaf(__uint_as_float(raw[4 * v + 1]), p.scale_log2, -l4.y));
-        pv[4 * v + 2] = fast_exp2(fmaf(__uint_as_float(raw[4 * v + 2]), p.scale_log2, -l4.z));
-        pv[4 * v + 3] = fast_exp2(fmaf(__uint_as_float(raw[4 * v + 3]), p.scale_log2, -l4.w));
+        pv[4 * v] = exp2_mixed(fmaf(__uint_as_float(raw[4 * v]), p.scale_log2, -l4.x), 0);
+        pv[4 * v + 1] = exp2_mixed(fmaf(__uint_as_float(raw[4 * v + 1]), p.scale_log2, -l4.y), 1);
+        pv[4 * v + 2] = exp2_mixed(fmaf(__uint_as_float(raw[4 * v + 2]), p.scale_log2, -l4.z), 2);
+        pv[4 * v + 3] = exp2_mixed(fmaf(__uint_as_float(raw[4 * v + 3]), p.scale_log2, -l4.w), 3);
       }
       if (need_mask) {  // diagonal tile (query < key) and the sequence tail
 #pragma unroll
@@ -743,7 +743,7 @@ __global__ void __launch_bounds__(320, 1)
       mbar_arrive(s_free);
       float pv[64];
 #pragma unroll
-      for (int i = 0; i < 64; ++i) pv[i] = fast_exp2(fmaf(__uint_as_float(raw[i]), p.scale_log2, -lse2));
+      for (int i = 0; i < 64; ++i) pv[i] = exp2_mixed(fmaf(__uint_as_float(raw[i]), p.scale_log2, -lse2), i);
       if (j == qt) {  // diagonal tile
 #pragma unroll
         for (int i = 0; i < 64; ++i)

@@ -62,6 +62,31 @@ HX_DEVICE float fast_exp2(float x) {
   return y;
 }
 
+// 2^x on the FMA pipe (no MUFU): x = n + f, f in [0,1); 2^f by a degree-3
+// minimax polynomial (max rel. error ~9e-5, below bf16's 2^-9 rounding of P);
+// 2^n added to the exponent field.  Valid for x <= 0 (softmax arguments);
+// clamped at -127 so the result flushes to ~0.  Used for a fraction of the
+// elements so the 16/clk/SM MUFU unit stops being the softmax floor (FA4).
+HX_DEVICE float exp2_poly(float x) {
+  x = fmaxf(x, -127.0f);
+  const float n = floorf(x);
+  const float f = x - n;
+  float p = fmaf(f, 0.0794402384f, 0.2244943373f);
+  p = fmaf(f, p, 0.6960656422f);
+  p = fmaf(f, p, 1.0f);
+  return __int_as_float(__float_as_int(p) + (static_cast<int>(n) << 23));
+}
+
+// Exponential of element k of an unrolled softmax row: every HX_POLY_EVERY-th
+// one is computed on the FMA pipe, the rest on MUFU (k is a compile-time
+// constant after unrolling, so the choice costs nothing).
+#ifndef HX_POLY_EVERY
+#define HX_POLY_EVERY 4
+#endif
+HX_DEVICE float exp2_mixed(float x, int k) {
+  return (HX_POLY_EVERY > 0 && k % HX_POLY_EVERY == HX_POLY_EVERY - 1) ? exp2_poly(x) : fast_exp2(x);
+}
+
 HX_DEVICE void named_barrier_sync(uint32_t id, uint32_t threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }

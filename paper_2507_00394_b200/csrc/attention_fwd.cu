@@ -179,8 +179,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
           uint32_t pk[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
-            const float e0 = fast_exp2(fmaf(__uint_as_float(raw[half * 64 + 2 * i]), c, neg_m));
-            const float e1 = fast_exp2(fmaf(__uint_as_float(raw[half * 64 + 2 * i + 1]), c, neg_m));
+            const float e0 = exp2_mixed(fmaf(__uint_as_float(raw[half * 64 + 2 * i]), c, neg_m), 2 * i);
+            const float e1 = exp2_mixed(fmaf(__uint_as_float(raw[half * 64 + 2 * i + 1]), c, neg_m), 2 * i + 1);
             rs += e0 + e1;
             pk[i] = pack_bf16(e0, e1);
           }

@@ -287,9 +287,7 @@ static int pick_bn(int M, int N, int num_sms) {
 
 cudaError_t gemm_launch(const GemmOperand& a, const GemmOperand& b, const GemmParams& p,
                         cudaStream_t stream) {
-  int dev = 0, num_sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+  const int num_sms = hx::num_sms();  // persistent grid size (honours HX_SM_RESERVE)
   const int bn = pick_bn(p.M, p.N, num_sms);
   CUtensorMap ta, tb;
   // A: K-major [M,K] box {64,128}; MN-major [K,M] box {64,64}

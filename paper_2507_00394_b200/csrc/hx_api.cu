@@ -10,6 +10,9 @@ namespace hx {
 
 static std::atomic<long long> g_launches{0};
 
+// SMs available to persistent kernels.  HX_SM_RESERVE (env) leaves SMs free for
+// concurrently running NCCL point-to-point kernels in multi-stage runs, so a
+// statically scheduled persistent GEMM never waits for a CTA slot.
 int num_sms() {
   static int n = 0;
   if (n == 0) {
@@ -17,6 +20,9 @@ int num_sms() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     if (n <= 0) n = 148;
+    const char* r = getenv("HX_SM_RESERVE");
+    const int reserve = r ? atoi(r) : 0;
+    if (reserve > 0 && reserve < n) n -= reserve;
   }
   return n;
 }

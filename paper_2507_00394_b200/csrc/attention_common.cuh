@@ -84,7 +84,11 @@ HX_DEVICE float exp2_poly(float x) {
 #define HX_POLY_EVERY 4
 #endif
 HX_DEVICE float exp2_mixed(float x, int k) {
-  return (HX_POLY_EVERY > 0 && k % HX_POLY_EVERY == HX_POLY_EVERY - 1) ? exp2_poly(x) : fast_exp2(x);
+  if constexpr (HX_POLY_EVERY > 0) {
+    constexpr int every = HX_POLY_EVERY > 0 ? HX_POLY_EVERY : 1;
+    if (k % every == every - 1) return exp2_poly(x);
+  }
+  return fast_exp2(x);
 }
 
 HX_DEVICE void named_barrier_sync(uint32_t id, uint32_t threads) {

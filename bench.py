@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-s", type=int, default=256)
+    ap.add_argument("--compare-1f1b", choices=["auto", "yes", "no"], default="auto",
+                    help="also time the same-kernel 1F1B schedule (default: only when N > 1)")
     return ap.parse_args()
 
 
@@ -214,6 +216,9 @@ def main() -> None:
     if args.impl == "reference":
         run_reference(args, wl, rank, world)
         return
+    if world > 1:
+        # leave SMs for the NCCL p2p kernels that run next to persistent GEMMs
+        os.environ.setdefault("HX_SM_RESERVE", "8")
 
     import torch
     import torch.distributed as dist
@@ -223,7 +228,7 @@ def main() -> None:
     from paper_2507_00394_b200.runtime import _lib, kernels as K
     from paper_2507_00394_b200.runtime.executor import DeviceModel, make_pair_groups, stage_fields
     from paper_2507_00394_b200.runtime.model import DeviceLayer, random_device_layer
-    from paper_2507_00394_b200.simulate import metrics_from_timeline
+    from paper_2507_00394_b200.simulate import measured_durations, metrics_from_timeline, simulate
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -231,27 +236,32 @@ def main() -> None:
         dist.init_process_group("nccl", device_id=dev)
     p = world
     cfg = ModelConfig(L=wl["L"], h=wl["h"], s=wl["s"], b=wl["b"], num_heads=wl["num_heads"], p=p, m=2 * p)
-    sched = generate(args.method, cfg, DurationTable.from_units(1, 3, 2))
+    units = DurationTable.from_units(1, 3, 2)
+    sched = generate(args.method, cfg, units)
     stages = [rank] if world > 1 else list(range(p))
-
-    # random-init weights of the architecture, drawn on the GPU (same distributions as make_model)
-    gen = torch.Generator(device=dev).manual_seed(1234)
-    layers = {}
-    for l in range(cfg.L):
-        need, own = set(), set()
-        for st in stages:
-            n_, o_ = stage_fields(sched, st, l)
-            need |= set(n_)
-            own |= set(o_)
-        full = random_device_layer(cfg.h, gen, dev)
-        if need:
-            layers[l] = DeviceLayer({k: v for k, v in full.items() if k in need},
-                                    tuple(k for k in full if k in own))
-        del full
-    model = DeviceModel(layers)
     groups = make_pair_groups(p) if world > 1 else None
-    rt = HelixRuntime(sched, model, args.mlp_chunk, "distributed" if world > 1 else "replay", dev,
-                      rank=rank if world > 1 else None, groups=groups)
+
+    def build_runtime(schedule):
+        """Random-init weights of the architecture, drawn on the GPU (same
+        distributions as make_model), placed per the schedule's stage ownership."""
+        gen = torch.Generator(device=dev).manual_seed(1234)
+        layers = {}
+        for l in range(cfg.L):
+            need, own = set(), set()
+            for st in stages:
+                n_, o_ = stage_fields(schedule, st, l)
+                need |= set(n_)
+                own |= set(o_)
+            full = random_device_layer(cfg.h, gen, dev)
+            if need:
+                layers[l] = DeviceLayer({k: v for k, v in full.items() if k in need},
+                                        tuple(k for k in full if k in own))
+            del full
+        return HelixRuntime(schedule, DeviceModel(layers), args.mlp_chunk,
+                            "distributed" if world > 1 else "replay", dev,
+                            rank=rank if world > 1 else None, groups=groups)
+
+    rt = build_runtime(sched)
     T = cfg.s * cfg.b
     ig = torch.Generator(device=dev).manual_seed(1)
     inputs = [torch.randn(T, cfg.h, generator=ig, device=dev).to(torch.bfloat16) for _ in range(cfg.m)]
@@ -261,26 +271,32 @@ def main() -> None:
             dist.barrier()
         torch.cuda.synchronize()
 
+    def time_steps(runtime, steps):
+        """Barrier + sync on both sides, CUDA events on the launching stream,
+        max over ranks.  Returns ms per step."""
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(steps):
+            runtime.run(inputs)
+        b.record()
+        barrier()
+        t_ms = a.elapsed_time(b) / steps
+        if world > 1:
+            t = torch.tensor([t_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            t_ms = float(t.item())
+        return t_ms
+
     for _ in range(args.warmup):
         rt.run(inputs)
     barrier()
     clocks = ClockSampler(local)
     clocks.start()
     launches0 = _lib.launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    e0.record()
-    for _ in range(args.steps):
-        rt.run(inputs)
-    e1.record()
-    barrier()
+    ms = time_steps(rt, args.steps)
     launches = _lib.launch_count() - launches0
-    ms = e0.elapsed_time(e1) / args.steps
     clk = clocks.stop()
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
     tokens = cfg.m * cfg.s * cfg.b
     value = tokens / (ms / 1e3)
     losses = rt.losses()
@@ -295,8 +311,31 @@ def main() -> None:
         allt = [None] * world
         dist.all_gather_object(allt, tl)
         tl = {k: v for part in allt for k, v in part.items()}
+    predicted = None
     if rank == 0 and tl:
-        bubble = metrics_from_timeline(sched, tl).bubble_fraction
+        measured = metrics_from_timeline(sched, tl)
+        bubble = measured.bubble_fraction
+        # the reference's own simulator fed with device-measured
+        # component times, predicted bubble / makespan next to the measured ones
+        sim = simulate(sched, measured_durations(sched, tl))
+        predicted = {"bubble_fraction": sim.metrics.bubble_fraction,
+                     "makespan_ms": sim.metrics.makespan / 1e6, "measured_makespan_ms": measured.makespan}
+
+    # same-kernel 1F1B baseline (the north-star comparison), same model / inputs
+    base_1f1b = None
+    if args.compare_1f1b == "yes" or (args.compare_1f1b == "auto" and world > 1):
+        del rt
+        torch.cuda.empty_cache()
+        rt_b = build_runtime(generate("1f1b", cfg, units))
+        for _ in range(max(1, args.warmup)):
+            rt_b.run(inputs)
+        ms_b = time_steps(rt_b, args.steps)
+        base_1f1b = {"value": tokens / (ms_b / 1e3), "ms_per_step": ms_b,
+                     "helix_speedup": ms_b / ms}
+        del rt_b
+        torch.cuda.empty_cache()
+        rt = build_runtime(sched)
+        rt.run(inputs)
 
     # e2e through the public runtime with host buffers
     e2e = None
@@ -385,6 +424,8 @@ def main() -> None:
             "mfu": value * fpt / (world * float(peaks["bf16_tflops"]) * 1e12),
             "model_flops_per_token": fpt,
             "bubble_fraction": bubble,
+            "bubble_predicted_by_reference_model": predicted,
+            "baseline_1f1b_same_kernels": base_1f1b,
             "losses": losses,
             "gpu_launches": launches,
             "e2e": e2e,

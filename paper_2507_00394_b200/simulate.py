@@ -79,6 +79,23 @@ def metrics_from_timeline(sched: Schedule, timeline, time_unit: str = "ms") -> M
     return Metrics(makespan, busy, bubble, frac, peaks, sends, time_unit)
 
 
+def measured_durations(sched: Schedule, timeline) -> DurationTable:
+    """Average device time per (component, pass) from a CUDA-event timeline, as a
+    ``DurationTable`` in integer nanoseconds.  Fused backward
+    tasks bill B and W together, so the W column is set to 0 and B carries both."""
+    sums: dict[tuple[str, str], list[float]] = {}
+    kinds = {"FWD": "fwd", "BWD_B": "bwd_b", "BWD_W": "bwd_w"}
+    for tid, (start, end) in timeline.items():
+        t = sched.tasks.get(tid)
+        if t is None or t.kind not in kinds or t.comp == "chunk":
+            continue
+        sums.setdefault((t.comp, kinds[t.kind]), []).append(end - start)
+    avg = {k: int(round(1e6 * sum(v) / len(v))) for k, v in sums.items()}  # ms -> ns
+    row = lambda comp: (avg.get((comp, "fwd"), 0), avg.get((comp, "bwd_b"), 0),  # noqa: E731
+                        avg.get((comp, "bwd_w"), 0))
+    return DurationTable.from_measured(row("pre"), row("attn"), row("post"))
+
+
 def simulate(sched: Schedule, durations: DurationTable, comm: CommModel | None = None) -> SimResult:
     fused = sched.meta.get("backward") == "fused"
     res = replay(sched, make_duration_fn(durations, fused), comm or CommModel.zero())

@@ -501,32 +501,41 @@ __global__ void __launch_bounds__(320, 1)
       constexpr uint32_t id_sp = idesc_bf16(128, 128, false, false);
       constexpr uint32_t id_kv = idesc_bf16(128, D, false, true);
       const uint32_t sk = smem_u32(smem + L::K), sv = smem_u32(smem + L::V);
-      mbar_wait(kv_full, 0);
-      for (int it = 0; it < n_it; ++it) {
-        const int st = it % ST;
-        const uint32_t sq = smem_u32(smem + L::Q + st * Tile<D>::BYTES);
-        const uint32_t sdo = smem_u32(smem + L::DO + st * Tile<D>::BYTES);
-        mbar_wait(&qdo_full[st], (it / ST) & 1);
+      auto sq = [&](int it) { return smem_u32(smem + L::Q + (it % ST) * Tile<D>::BYTES); };
+      auto sdo = [&](int it) { return smem_u32(smem + L::DO + (it % ST) * Tile<D>::BYTES); };
+      auto issue_s = [&](int it) {  // S^T(it): the S region is free once dV(it-1) was issued
+        mbar_wait(&qdo_full[it % ST], (it / ST) & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
-          umma_f16_ss(tS, kdesc(sk, kk, AT_TILE), kdesc(sq, kk, AT_TILE), id_sp, kk > 0);
+          umma_f16_ss(tS, kdesc(sk, kk, AT_TILE), kdesc(sq(it), kk, AT_TILE), id_sp, kk > 0);
         umma_commit(s_full);
+      };
+      auto issue_dp = [&](int it) {  // dP^T(it): the dP region is free once dK(it-1) was issued
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
-          umma_f16_ss(tDP, kdesc(sv, kk, AT_TILE), kdesc(sdo, kk, AT_TILE), id_sp, kk > 0);
+          umma_f16_ss(tDP, kdesc(sv, kk, AT_TILE), kdesc(sdo(it), kk, AT_TILE), id_sp, kk > 0);
         umma_commit(dp_full);
+      };
+      mbar_wait(kv_full, 0);
+      issue_s(0);
+      issue_dp(0);
+      // Stream: dV(i) | S^T(i+1) | dK(i) | dP^T(i+1).  S^T(i+1) only waits for P^T(i)
+      // (consumed by dV(i)), so the next softmax starts while dK(i) and dP^T(i+1) run.
+      for (int it = 0; it < n_it; ++it) {
         mbar_wait(p_full, it & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < AT_TILE / 16; ++kk)
-          umma_f16_ts(tDV, packed_kstep<64>(tS, kk), mndesc(sdo, kk, AT_TILE), id_kv, it > 0 || kk > 0);
+          umma_f16_ts(tDV, packed_kstep<64>(tS, kk), mndesc(sdo(it), kk, AT_TILE), id_kv, it > 0 || kk > 0);
+        if (it + 1 < n_it) issue_s(it + 1);
         mbar_wait(ds_full, it & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < AT_TILE / 16; ++kk)
-          umma_f16_ts(tDK, packed_kstep<64>(tDP, kk), mndesc(sq, kk, AT_TILE), id_kv, it > 0 || kk > 0);
-        umma_commit(&qdo_empty[st]);
+          umma_f16_ts(tDK, packed_kstep<64>(tDP, kk), mndesc(sq(it), kk, AT_TILE), id_kv, it > 0 || kk > 0);
+        umma_commit(&qdo_empty[it % ST]);
+        if (it + 1 < n_it) issue_dp(it + 1);
       }
       umma_commit(acc_full);
     }

@@ -228,7 +228,7 @@ def main() -> None:
     from paper_2507_00394_b200.runtime import _lib, kernels as K
     from paper_2507_00394_b200.runtime.executor import DeviceModel, make_pair_groups, stage_fields
     from paper_2507_00394_b200.runtime.model import DeviceLayer, random_device_layer
-    from paper_2507_00394_b200.simulate import measured_durations, metrics_from_timeline, simulate
+    from paper_2507_00394_b200.simulate import measured_durations, metrics_from_timeline, predict_pipeline, simulate
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -317,9 +317,14 @@ def main() -> None:
         bubble = measured.bubble_fraction
         # the reference's own simulator fed with device-measured
         # component times, predicted bubble / makespan next to the measured ones
-        sim = simulate(sched, measured_durations(sched, tl))
+        table = measured_durations(sched, tl)
+        sim = simulate(sched, table)
         predicted = {"bubble_fraction": sim.metrics.bubble_fraction,
                      "makespan_ms": sim.metrics.makespan / 1e6, "measured_makespan_ms": measured.makespan}
+        if world == 1:
+            # helix vs same-kernel 1F1B at p = 2/4/8 predicted from these measured component
+            # times (reference simulator, NVLink 770 GB/s per direction): a prediction only
+            predicted["pipeline_prediction"] = predict_pipeline(cfg, table)
 
     # same-kernel 1F1B baseline (the north-star comparison), same model / inputs
     base_1f1b = None

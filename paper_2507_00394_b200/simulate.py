@@ -96,6 +96,38 @@ def measured_durations(sched: Schedule, timeline) -> DurationTable:
     return DurationTable.from_measured(row("pre"), row("attn"), row("post"))
 
 
+def predict_pipeline(cfg, durations: DurationTable, stages=(2, 4, 8), link_gbs: float = 770.0,
+                     latency_us: float = 5.0, methods=("helix_twofold", "helix_twofold_rc", "1f1b")) -> dict:
+    """Predicted throughput of each method at p stages (m = 2p, weak scaling),
+    from measured per-component durations (ns) and an NVLink transfer model
+    (bytes over ``link_gbs`` per direction + latency) in the reference's own
+    list-scheduling simulator (``P/simulate.py:54-75``).  A prediction, not a
+    measurement: it shows where the measured kernels put the helix-vs-1F1B ratio."""
+    from .engine import CommModel
+    from .generators import generate
+
+    comm = CommModel("bytes", latency=int(latency_us * 1000), bytes_per_element=2,
+                     bandwidth=int(link_gbs * 1e9))
+    out = {}
+    for p in stages:
+        if cfg.L % p:
+            continue
+        c = cfg.with_(p=p, m=2 * p)
+        row = {}
+        for method in methods:
+            res = simulate(generate(method, c, durations), durations, comm)
+            tokens = c.m * c.s * c.b
+            row[method] = {"tokens_per_s": tokens / (res.metrics.makespan * 1e-9),
+                           "bubble_fraction": res.metrics.bubble_fraction,
+                           "makespan_ms": res.metrics.makespan / 1e6}
+        if "1f1b" in row:
+            for method in methods:
+                if method != "1f1b":
+                    row[method]["speedup_vs_1f1b"] = (row["1f1b"]["makespan_ms"] / row[method]["makespan_ms"])
+        out[f"p{p}"] = row
+    return out
+
+
 def simulate(sched: Schedule, durations: DurationTable, comm: CommModel | None = None) -> SimResult:
     fused = sched.meta.get("backward") == "fused"
     res = replay(sched, make_duration_fn(durations, fused), comm or CommModel.zero())

@@ -573,14 +573,32 @@ class _Distributed:
             raise ExecutionError(f"undelivered payloads: {sorted(self.posted)}")
 
 
-def make_pair_groups(n_stages: int) -> dict[tuple[int, int], object]:
+def make_pair_groups(n_stages: int, warm: bool = True, device=None) -> dict[tuple[int, int], object]:
     """One 2-rank group per directed stage pair; every rank must call this in
-    the same order (``torch.distributed.new_group`` is collective)."""
+    the same order (``torch.distributed.new_group`` is collective).
+
+    With ``warm`` each group's point-to-point communicator is created right
+    away by one tiny send/recv, walking the groups in the same global order on
+    every rank.  NCCL creates p2p communicators lazily and the creation blocks
+    the host until the peer joins, so first touching pairs in rank-dependent
+    order inside the schedule could deadlock two hosts; a single total order
+    over all groups cannot."""
     groups = {}
     for a in range(n_stages):
         for b in range(n_stages):
             if a != b:
                 groups[(a, b)] = torch.distributed.new_group([a, b])
+    if warm:
+        rank = torch.distributed.get_rank()
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device()) \
+                if torch.distributed.get_backend() == "nccl" else torch.device("cpu")
+        token = torch.zeros(1, device=device)
+        for (a, b), grp in groups.items():
+            if rank == a:
+                torch.distributed.send(token, dst=b, group=grp)
+            elif rank == b:
+                torch.distributed.recv(token, src=a, group=grp)
     return groups
 
 

@@ -91,6 +91,76 @@ HX_DEVICE float exp2_mixed(float x, int k) {
   return fast_exp2(x);
 }
 
+// Packed two-wide fp32 arithmetic (sm_100 FFMA2 / FADD2 / FMUL2) and the
+// three-input max (FMNMX3): half the issue slots for the softmax element math.
+HX_DEVICE uint64_t f2pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+HX_DEVICE float2 f2unpack(uint64_t r) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+  return make_float2(a, b);
+}
+HX_DEVICE uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+HX_DEVICE uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+HX_DEVICE uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+HX_DEVICE float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+// bf16x2 of exp2 of a packed pair
+HX_DEVICE uint32_t exp2_pack(uint64_t x2, float& s0, float& s1) {
+  const float2 x = f2unpack(x2);
+  s0 = fast_exp2(x.x);
+  s1 = fast_exp2(x.y);
+  return pack_bf16(s0, s1);
+}
+
+// exp2 of a packed pair on the FMA pipe (no MUFU): n = round(x) via the 1.5*2^23
+// magic add, f = x - n in [-0.5, 0.5], 2^f by a degree-3 relative-minimax
+// polynomial (max rel. error 7.5e-5, far below bf16's 2^-9 rounding of P), 2^n
+// added to the exponent field.  x <= 0 (softmax arguments); clamped at -125 so
+// the exponent sum never wraps (2^f can sit just below 1 with n = -125).
+HX_DEVICE uint32_t exp2_pack_poly(uint64_t x2, float& s0, float& s1) {
+  const float2 xu = f2unpack(x2);
+  const uint64_t x = f2pack(fmaxf(xu.x, -125.f), fmaxf(xu.y, -125.f));
+  constexpr float MAGIC = 12582912.f;
+  const uint64_t j = fadd2(x, f2pack(MAGIC, MAGIC));
+  const uint64_t f = fadd2(x, fadd2(f2pack(MAGIC, MAGIC), j ^ 0x8000000080000000ull));
+  uint64_t q = ffma2(f, f2pack(0.0551716536f, 0.0551716536f), f2pack(0.242611155f, 0.242611155f));
+  q = ffma2(f, q, f2pack(0.693260968f, 0.693260968f));
+  q = ffma2(f, q, f2pack(0.999928057f, 0.999928057f));
+  const float2 qf = f2unpack(q), jf = f2unpack(j);
+  s0 = __int_as_float(__float_as_int(qf.x) + (__float_as_int(jf.x) << 23));
+  s1 = __int_as_float(__float_as_int(qf.y) + (__float_as_int(jf.y) << 23));
+  return pack_bf16(s0, s1);
+}
+
+// Pair i of an unrolled softmax row: every HX_POLY_EVERY-th pair on the FMA pipe.
+// (i is a compile-time constant after unrolling, so the choice costs nothing.)
+HX_DEVICE uint32_t exp2_pack_mixed(uint64_t x2, int i, float& s0, float& s1) {
+  if constexpr (HX_POLY_EVERY > 0) {
+    constexpr int every = HX_POLY_EVERY > 0 ? HX_POLY_EVERY : 1;
+    if (i % every == every - 1) return exp2_pack_poly(x2, s0, s1);
+  }
+  return exp2_pack(x2, s0, s1);
+}
+
 HX_DEVICE void named_barrier_sync(uint32_t id, uint32_t threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }

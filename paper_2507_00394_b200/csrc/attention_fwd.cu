@@ -11,7 +11,7 @@
 //   O += P V     TS-MMA (A = P from TMEM, B = V MN-major from smem) -> TMEM O_g
 // O is rescaled only when a row's running max grows by more than 2^8 (exponents
 // stay <= 256, exact in fp32), so rescales are rare after the first tiles.
-// Warp 8 issues TMA (Q once, K/V double-buffered), warp 9 issues MMAs and owns TMEM.
+// Warp 8 issues TMA (Q once, K/V through a 5-slot ring), warp 9 issues MMAs and owns TMEM.
 // TMEM (512 columns): S_A 0-127 | S_B 128-255 | O_A 256-383 | O_B 384-511.
 #include "attention_common.cuh"
 
@@ -19,30 +19,45 @@ namespace hx {
 
 constexpr int FWD_THREADS = 320;
 
+// Debug build only (-DHX_FWD_TRACE): clock64 stamps of CTA (0,0)'s pipeline
+// events, read back with hx_debug_fwd_trace (tools/fwd_trace.py).
+#ifdef HX_FWD_TRACE
+__device__ long long g_fwd_trace[8][1024];
+#define HX_TR(slot, idx) \
+  if (blockIdx.x == 0 && blockIdx.y == 0 && (idx) < 1024) g_fwd_trace[slot][idx] = clock64()
+#else
+#define HX_TR(slot, idx)
+#endif
+
 template <int D>
 struct FwdSmem {
+  // K and V tiles share one ring, in load order K(0) V(0) K(1) V(1) ...; as many
+  // slots as fit next to the two Q tiles (5 at d=128), so the TMA loads of
+  // K/V(j+1) are in flight during the whole of step j.
+  static constexpr int NSLOT_FIT = (227 * 1024 - 2 * Tile<D>::BYTES - 512) / Tile<D>::BYTES;
+  static constexpr int NSLOT = NSLOT_FIT > 8 ? 8 : NSLOT_FIT;
   static constexpr int QA = 0;
   static constexpr int QB = QA + Tile<D>::BYTES;
-  static constexpr int KV = QB + Tile<D>::BYTES;  // 2 stages x (K, V)
-  static constexpr int BAR = KV + 4 * Tile<D>::BYTES;
-  static constexpr int TOTAL = BAR + 256;
+  static constexpr int KV = QB + Tile<D>::BYTES;
+  static constexpr int BAR = KV + NSLOT * Tile<D>::BYTES;
+  static constexpr int TOTAL = BAR + 512;
 };
 
 template <int D>
 __global__ void __launch_bounds__(FWD_THREADS, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const AttnParams p) {
   using L = FwdSmem<D>;
+  constexpr int NS = L::NSLOT;
   extern __shared__ __align__(1024) uint8_t smem[];
   if ((smem_u32(smem) & 1023) != 0) __trap();
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR);
-  uint64_t* q_full = bars;          // 1
-  uint64_t* k_full = bars + 1;      // 2
-  uint64_t* v_full = bars + 3;      // 2
-  uint64_t* kv_empty = bars + 5;    // 2
-  uint64_t* s_full = bars + 7;      // 2 (per group)
-  uint64_t* p_full = bars + 9;      // 2, 128 arrivals each
-  uint64_t* o_full = bars + 11;     // 2
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
+  uint64_t* q_full = bars;               // 1
+  uint64_t* s_full = bars + 1;           // 2 (per group)
+  uint64_t* p_full = bars + 3;           // 2, 128 arrivals each
+  uint64_t* o_full = bars + 5;           // 2
+  uint64_t* kv_full = bars + 7;          // NS
+  uint64_t* kv_empty = bars + 7 + NS;    // NS
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 7 + 2 * NS);
 
   const int warp = warp_id(), lane = lane_id();
   const int nq = (p.s + AT_TILE - 1) / AT_TILE;
@@ -58,7 +73,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 
   if (warp == 8 && lane == 0) {
     tma_prefetch(&tm_qkv);
-    for (int i = 0; i < 13; ++i) mbar_init(&bars[i], (i == 9 || i == 10) ? 128 : 1);
+    for (int i = 0; i < 7 + 2 * NS; ++i) mbar_init(&bars[i], (i == 3 || i == 4) ? 128 : 1);
     fence_barrier_init();
   }
   if (warp == 9) tmem_alloc(tmem_slot, 512);
@@ -66,20 +81,20 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // ring slot n: K(n/2) for even n, V(n/2) for odd n
+  auto slot_addr = [&](int n) { return smem + L::KV + (n % NS) * Tile<D>::BYTES; };
 
   if (warp == 8) {
     if (lane == 0) {  // ---------------- TMA producer
       mbar_arrive_expect_tx(q_full, (has_b ? 2 : 1) * Tile<D>::BYTES);
       tma_tile_rows<D>(smem + L::QA, &tm_qkv, q_full, qcol, bi, qtile[0] * AT_TILE, AT_TILE);
       if (has_b) tma_tile_rows<D>(smem + L::QB, &tm_qkv, q_full, qcol, bi, qtile[1] * AT_TILE, AT_TILE);
-      for (int j = 0; j < nkv; ++j) {
-        const int st = j & 1;
-        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
-        uint8_t* kb = smem + L::KV + st * 2 * Tile<D>::BYTES;
-        mbar_arrive_expect_tx(&k_full[st], Tile<D>::BYTES);
-        tma_tile_rows<D>(kb, &tm_qkv, &k_full[st], kcol, bi, j * AT_TILE, AT_TILE);
-        mbar_arrive_expect_tx(&v_full[st], Tile<D>::BYTES);
-        tma_tile_rows<D>(kb + Tile<D>::BYTES, &tm_qkv, &v_full[st], vcol, bi, j * AT_TILE, AT_TILE);
+      for (int n = 0; n < 2 * nkv; ++n) {
+        const int sl = n % NS;
+        mbar_wait(&kv_empty[sl], ((n / NS) & 1) ^ 1);
+        mbar_arrive_expect_tx(&kv_full[sl], Tile<D>::BYTES);
+        tma_tile_rows<D>(slot_addr(n), &tm_qkv, &kv_full[sl], (n & 1) ? vcol : kcol, bi, (n >> 1) * AT_TILE,
+                         AT_TILE);
       }
     }
   } else if (warp == 9) {
@@ -89,36 +104,45 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       const uint32_t sq[2] = {smem_u32(smem + L::QA), smem_u32(smem + L::QB)};
       bool pending[2] = {false, false};
       int pcount[2] = {0, 0};
+      auto wait_slot = [&](int n) {
+        mbar_wait(&kv_full[n % NS], (n / NS) & 1);
+        tc_fence_after();
+      };
       mbar_wait(q_full, 0);
       auto issue_pv = [&](int g, int jt) {  // O_g += P_g(jt) V(jt)
+        wait_slot(2 * jt + 1);
         mbar_wait(&p_full[g], pcount[g] & 1);
         ++pcount[g];
-        mbar_wait(&v_full[jt & 1], (jt >> 1) & 1);
         tc_fence_after();
-        const uint32_t sv = smem_u32(smem + L::KV + (jt & 1) * 2 * Tile<D>::BYTES + Tile<D>::BYTES);
+        const uint32_t sv = smem_u32(slot_addr(2 * jt + 1));
         const uint32_t tP = tmem + 128 * g, tO = tmem + 256 + 128 * g;
+        HX_TR(2, 2 * jt + g);
 #pragma unroll
         for (int kk = 0; kk < AT_TILE / 16; ++kk)
           umma_f16_ts(tO, tP + kk * 8, mndesc(sv, kk, AT_TILE), id_o, (jt > 0 || kk > 0));
         pending[g] = false;
       };
       for (int j = 0; j < nkv; ++j) {
-        mbar_wait(&k_full[j & 1], (j >> 1) & 1);
-        tc_fence_after();
-        const uint32_t sk = smem_u32(smem + L::KV + (j & 1) * 2 * Tile<D>::BYTES);
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
-          if (pending[g]) issue_pv(g, j - 1);
+          // PV_g(j-1) only needs V(j-1): issue it before waiting for K(j)
+          if (pending[g]) {
+            issue_pv(g, j - 1);
+            if (g == 1 || !pending[1]) umma_commit(&kv_empty[(2 * j - 1) % NS]);  // V(j-1) free
+          }
           if (j <= last[g]) {  // S_g(j) = Q_g K(j)^T
+            wait_slot(2 * j);
+            const uint32_t sk = smem_u32(slot_addr(2 * j));
             const uint32_t tS = tmem + 128 * g;
 #pragma unroll
             for (int kk = 0; kk < D / 16; ++kk)
               umma_f16_ss(tS, kdesc(sq[g], kk, AT_TILE), kdesc(sk, kk, AT_TILE), id_s, kk > 0);
             umma_commit(&s_full[g]);
+            HX_TR(3, 2 * j + g);
             pending[g] = true;
           }
         }
-        if (j > 0) umma_commit(&kv_empty[(j - 1) & 1]);
+        umma_commit(&kv_empty[(2 * j) % NS]);  // K(j) free
       }
       for (int g = 0; g < 2; ++g)
         if (pending[g]) issue_pv(g, last[g]);
@@ -139,24 +163,27 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       float m_used = -INFINITY, l_run = 0.f;
       for (int j = 0; j <= qt; ++j) {
         mbar_wait(&s_full[g], j & 1);
+        if (quad == 0 && lane == 0) HX_TR(g, 2 * j);
         tc_fence_after();
         uint32_t raw[AT_TILE];
 #pragma unroll
         for (int ch = 0; ch < AT_TILE / 32; ++ch)
           tmem_ld32(tS + ch * 32, *reinterpret_cast<uint32_t(*)[32]>(raw + ch * 32));
         tmem_wait_ld();
-        float mx = -INFINITY;
+        if (quad == 0 && lane == 0) HX_TR(4 + g, j);
         if (j == qt) {  // diagonal tile: key index > query index is masked
 #pragma unroll
-          for (int i = 0; i < AT_TILE; ++i) {
+          for (int i = 0; i < AT_TILE; ++i)
             if (i > r) raw[i] = __float_as_uint(-INFINITY);
-            mx = fmaxf(mx, __uint_as_float(raw[i]));
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < AT_TILE; ++i) mx = fmaxf(mx, __uint_as_float(raw[i]));
         }
-        mx *= c;
+        // row max: four independent 3-input-max chains
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int i = 0; i < AT_TILE; i += 8)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            m4[k] = fmax3(m4[k], __uint_as_float(raw[i + 2 * k]), __uint_as_float(raw[i + 2 * k + 1]));
+        float mx = fmax3(m4[0], m4[1], fmaxf(m4[2], m4[3])) * c;
         const float m_new = (mx > m_used + 8.0f) ? mx : m_used;
         const float alpha = fast_exp2(m_used - m_new);
         if (j > 0 && __any_sync(0xffffffffu, m_new != m_used)) {
@@ -172,24 +199,29 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
           }
         }
         m_used = m_new;
-        const float neg_m = -m_new;
-        float rs = 0.f;
+        if (quad == 0 && lane == 0) HX_TR(6 + g, j);
+        // p = 2^(s*c - m) on packed pairs (FFMA2), row sum on packed pairs (FADD2)
+        const uint64_t c2 = f2pack(c, c), nm2 = f2pack(-m_new, -m_new);
+        uint64_t rs2[2] = {f2pack(0.f, 0.f), f2pack(0.f, 0.f)};
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
           uint32_t pk[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
-            const float e0 = exp2_mixed(fmaf(__uint_as_float(raw[half * 64 + 2 * i]), c, neg_m), 2 * i);
-            const float e1 = exp2_mixed(fmaf(__uint_as_float(raw[half * 64 + 2 * i + 1]), c, neg_m), 2 * i + 1);
-            rs += e0 + e1;
-            pk[i] = pack_bf16(e0, e1);
+            const uint64_t x2 = ffma2(f2pack(__uint_as_float(raw[half * 64 + 2 * i]),
+                                             __uint_as_float(raw[half * 64 + 2 * i + 1])), c2, nm2);
+            float e0, e1;
+            pk[i] = exp2_pack_mixed(x2, i, e0, e1);
+            rs2[i & 1] = fadd2(rs2[i & 1], f2pack(e0, e1));
           }
           tmem_st32(tS + half * 32, pk);  // P over the first 64 columns of S
         }
         tmem_wait_st();
-        l_run = l_run * alpha + rs;
+        const float2 ra = f2unpack(rs2[0]), rb = f2unpack(rs2[1]);
+        l_run = l_run * alpha + ((ra.x + ra.y) + (rb.x + rb.y));
         tc_fence_before();
         mbar_arrive(&p_full[g]);
+        if (quad == 0 && lane == 0) HX_TR(g, 2 * j + 1);
       }
       mbar_wait(&o_full[g], 0);
       tc_fence_after();
@@ -207,6 +239,12 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     tmem_dealloc(tmem, 512);
   }
 }
+
+#ifdef HX_FWD_TRACE
+extern "C" HX_API int hx_debug_fwd_trace(long long* out) {
+  return static_cast<int>(cudaMemcpyFromSymbol(out, g_fwd_trace, sizeof(g_fwd_trace)));
+}
+#endif
 
 template <int D>
 static cudaError_t fwd_launch(const void* qkv, int ld_qkv, const AttnParams& p, cudaStream_t st) {

@@ -785,6 +785,414 @@ __global__ void __launch_bounds__(320, 1)
   }
 }
 
+// ------------------------------------------------------------------ fused (v10)
+// One pass, CTA = one 128-row key tile of one (batch, head); streams 128-row
+// query tiles i from the diagonal to the end.  dK and dV stay in TMEM for the
+// CTA's lifetime; the partial dQ(i) = dS(i) K of every tile is reduced into an
+// fp32 accumulator in global memory by TMA bulk reduce-adds (L2 does the adds),
+// so the score / dP matmuls and the exponentials are done once (5 MMAs per tile
+// pair instead of the split kernels' 7).  MMA stream per tile:
+//   dV(i) += P^T dO | dP^T(i) = V dO^T | S^T(i+1) = K Q^T | dK += dS^T Q | dQ(i) = dS K
+//   (P^T written over S^T, dS^T over dP^T in TMEM; dS also to smem as dQ's A operand.)
+// TMEM (D=128): dK 0 | dV 128 | S^T 256 | dP^T 384, dQ(i) over dP^T once dK(i)
+//   has read dS^T (the tensor pipe runs in issue order); the reduce warpgroup
+//   drains dQ(i) while dV(i+1) runs.  D=64: dQ gets its own columns at 384.
+// Warps: 0-7 compute (thread = key row, warpgroup g owns query columns 64g..),
+//   8 TMA, 9 MMA, 10-11 idle, 12-15 dQ reduce (thread = query row).
+// Debug-only ablations for pipeline analysis (tools/bwd_trace.py): skip the
+// softmax math (NOCOMPUTE) or the dQ staging / reduce-add (NOREDUCE).
+#ifdef HX_BWD_NOCOMPUTE
+constexpr bool kNoCompute = true;
+#else
+constexpr bool kNoCompute = false;
+#endif
+#ifdef HX_BWD_NOREDUCE
+constexpr bool kNoReduce = true;
+#else
+constexpr bool kNoReduce = false;
+#endif
+
+#ifdef HX_BWD_TRACE
+// Debug build only: clock64 per event and iteration for CTA (0, 0) (the key tile
+// with the most query tiles), read back with hx_debug_bwd_trace (tools/bwd_trace.py).
+__device__ long long g_bwd_trace[16][512];
+#define HX_BT(slot, idx) \
+  if (blockIdx.x == 0 && blockIdx.y == 0 && (idx) < 512) g_bwd_trace[slot][idx] = clock64()
+#else
+#define HX_BT(slot, idx)
+#endif
+
+template <int D>
+struct FusedSmem {
+  static constexpr int K = 0;
+  static constexpr int V = K + Tile<D>::BYTES;
+  static constexpr int Q = V + Tile<D>::BYTES;               // 2 x [128 x D]
+  static constexpr int DO = Q + 2 * Tile<D>::BYTES;          // [128 x D]
+  static constexpr int DS = DO + Tile<D>::BYTES;             // [128 keys x 128 q], MN-major A of dQ
+  static constexpr int STG = DS + AT_TILE * AT_TILE * 2;     // 2 x [128 x 32] fp32 reduce staging
+  static constexpr int STAT = STG + 2 * AT_TILE * 32 * 4;    // [2][-lse2 | -delta][128]
+  static constexpr int BAR = STAT + 2 * 2 * AT_TILE * 4;
+  static constexpr int TOTAL = BAR + 256;
+};
+
+template <int D, bool RED>
+__global__ void __launch_bounds__(512, 1)
+    attn_bwd_fused_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                          const __grid_constant__ CUtensorMap tm_dq, float* __restrict__ dq_acc, const AttnParams p) {
+  using L = FusedSmem<D>;
+  constexpr int NT = 256;  // compute threads
+  constexpr bool DQ_SHARES_DP = 2 * D + 256 + D > 512;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if ((smem_u32(smem) & 1023) != 0) __trap();
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR);
+  uint64_t* q_full = bars;        // 2
+  uint64_t* q_empty = bars + 2;   // 2
+  uint64_t* kv_full = bars + 4;
+  uint64_t* do_full = bars + 5;
+  uint64_t* do_empty = bars + 6;
+  uint64_t* s_full = bars + 7;
+  uint64_t* p_full = bars + 8;    // NT arrivals
+  uint64_t* dp_full = bars + 9;
+  uint64_t* ds_full = bars + 10;  // NT arrivals
+  uint64_t* dq_full = bars + 11;
+  uint64_t* dq_empty = bars + 12; // 128 arrivals
+  uint64_t* acc_full = bars + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  constexpr int NBARS = 14;
+  float* stat = reinterpret_cast<float*>(smem + L::STAT);
+
+  const int warp = warp_id(), lane = lane_id();
+  const int nq = (p.s + AT_TILE - 1) / AT_TILE;
+  const int kt = static_cast<int>(blockIdx.x);  // heaviest key tiles first
+  const int bh = blockIdx.y;
+  const int bi = bh / p.heads, head = bh % p.heads;
+  const int qcol = head * D, kcol = p.h + head * D, vcol = 2 * p.h + head * D;
+  const int n_it = nq - kt;
+
+  if (warp == 8 && lane == 0) {
+    tma_prefetch(&tm_qkv);
+    tma_prefetch(&tm_do);
+    tma_prefetch(&tm_dq);
+    for (int i = 0; i < NBARS; ++i) mbar_init(&bars[i], (i == 8 || i == 10) ? NT : (i == 12 ? 128 : 1));
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tDK = tmem, tDV = tmem + D, tS = tmem + 2 * D, tDP = tmem + 2 * D + 128;
+  const uint32_t tDQ = DQ_SHARES_DP ? tDP : tmem + 2 * D + 256;
+
+  // Each role ends the kernel itself (no code shared after the role branches,
+  // so ptxas can allocate each branch under its own setmaxnreg budget).
+  auto finish = [&]() {
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 9) {
+      tc_fence_after();
+      tmem_dealloc(tmem, 512);
+    }
+  };
+  if (warp >= 8 && warp < 12) {
+    regs_dec<104>();
+    if (warp == 8 && lane == 0) {
+      mbar_arrive_expect_tx(kv_full, 2 * Tile<D>::BYTES);
+      tma_tile_rows<D>(smem + L::K, &tm_qkv, kv_full, kcol, bi, kt * AT_TILE, AT_TILE);
+      tma_tile_rows<D>(smem + L::V, &tm_qkv, kv_full, vcol, bi, kt * AT_TILE, AT_TILE);
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it & 1, q0 = (kt + it) * AT_TILE;
+        mbar_wait(&q_empty[st], ((it >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&q_full[st], Tile<D>::BYTES);
+        tma_tile_rows<D>(smem + L::Q + st * Tile<D>::BYTES, &tm_qkv, &q_full[st], qcol, bi, q0, AT_TILE);
+        mbar_wait(do_empty, (it & 1) ^ 1);
+        mbar_arrive_expect_tx(do_full, Tile<D>::BYTES);
+        tma_tile_rows<D>(smem + L::DO, &tm_do, do_full, head * D, bi, q0, AT_TILE);
+      }
+    } else if (warp == 9) {
+      // The whole warp runs the issue loop (warp-uniform descriptors on the uniform
+      // datapath); one elected lane issues each tcgen05 instruction.  Fully unrolled
+      // chains: the tensor pipe's queue is shallow, so per-MMA issue cost must stay
+      // well below the 64-cycle MMA time.
+      constexpr uint32_t id_s = idesc_bf16(128, 128, false, false);  // S^T, dP^T: K-major x K-major
+      constexpr uint32_t id_kv = idesc_bf16(128, D, false, true);    // dV, dK: TMEM A x MN-major B
+      constexpr uint32_t id_dq = idesc_bf16(128, D, true, true);     // dQ: MN-major dS x MN-major K
+      const uint32_t sk = smem_u32(smem + L::K), sv = smem_u32(smem + L::V);
+      const uint32_t sdo = smem_u32(smem + L::DO), sds = smem_u32(smem + L::DS);
+      auto sq = [&](int it) { return smem_u32(smem + L::Q + (it & 1) * Tile<D>::BYTES); };
+      auto mma_kk = [&](uint32_t d, uint32_t a_smem, uint32_t b_smem, uint32_t id) {
+        // K-major x K-major over K = D: per 64-column atom, four 16-wide steps (+32 B)
+        const uint64_t da = sw128_desc(a_smem, 16, 1024), db = sw128_desc(b_smem, 16, 1024);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = ((kk >> 2) * AT_TILE * 128 + (kk & 3) * 32) >> 4;
+          umma_f16_ss_e(d, da + off, db + off, id, kk > 0);
+        }
+      };
+      auto mma_ts_mn = [&](uint32_t d, uint32_t a_tmem, uint32_t b_smem, uint32_t id, bool acc) {
+        // TMEM A (packed, 64-column groups) x MN-major B over K = 128 rows (+2048 B per step)
+        const uint64_t db = sw128_desc(b_smem, AT_TILE * 128, 1024);
+#pragma unroll
+        for (int kk = 0; kk < AT_TILE / 16; ++kk)
+          umma_f16_ts_e(d, a_tmem + 64 * (kk >> 2) + 8 * (kk & 3), db + 128 * kk, id, acc || kk > 0);
+      };
+      auto issue_s = [&](int it) {
+        mbar_wait(&q_full[it & 1], (it >> 1) & 1);
+        tc_fence_after();
+        mma_kk(tS, sk, sq(it), id_s);
+        umma_commit_e(s_full);
+      };
+      auto issue_dp = [&]() {
+        mma_kk(tDP, sv, sdo, id_s);
+        umma_commit_e(dp_full);
+      };
+      // Stream per tile: dP^T(i) was issued at the end of tile i-1 (as soon as dQ(i-1)
+      // left the shared TMEM columns), so it runs while the softmax builds P^T(i):
+      //   dV(i) | S^T(i+1) | dK(i) | dQ(i) | dP^T(i+1)
+      mbar_wait(kv_full, 0);
+      issue_s(0);
+      mbar_wait(do_full, 0);
+      tc_fence_after();
+      issue_dp();
+      const uint64_t dq_a = sw128_desc(sds, AT_TILE * 128, 1024), dq_b = sw128_desc(sk, AT_TILE * 128, 1024);
+      for (int it = 0; it < n_it; ++it) {
+        mbar_wait(p_full, it & 1);
+        tc_fence_after();
+        HX_BT(0, it);
+        mma_ts_mn(tDV, tS, sdo, id_kv, it > 0);
+        umma_commit_e(do_empty);  // dO(it) read by dP^T(it) and dV(it)
+        if (it + 1 < n_it) issue_s(it + 1);
+        HX_BT(2, it);
+        mbar_wait(ds_full, it & 1);
+        tc_fence_after();
+        HX_BT(3, it);
+        mma_ts_mn(tDK, tDP, sq(it), id_kv, it > 0);
+        umma_commit_e(&q_empty[it & 1]);
+        if (!DQ_SHARES_DP && it > 0) {
+          mbar_wait(dq_empty, (it - 1) & 1);
+          tc_fence_after();
+        }
+        HX_BT(4, it);
+#pragma unroll
+        for (int kk = 0; kk < AT_TILE / 16; ++kk) umma_f16_ss_e(tDQ, dq_a + 128 * kk, dq_b + 128 * kk, id_dq, kk > 0);
+        umma_commit_e(dq_full);
+        if (it + 1 < n_it) {
+          mbar_wait(do_full, (it + 1) & 1);
+          if (DQ_SHARES_DP) mbar_wait(dq_empty, it & 1);  // dQ(it) drained from the dP columns
+          tc_fence_after();
+          HX_BT(1, it + 1);
+          issue_dp();
+        }
+      }
+      umma_commit_e(acc_full);
+    }
+    finish();
+    return;
+  } else if (warp >= 12) {
+    // dQ reduce: thread = query row r of the current tile; TMEM -> registers ->
+    // swizzled smem staging -> TMA reduce-add into the fp32 accumulator.
+    regs_inc<136>();
+    const int quad = warp & 3, r = quad * 32 + lane, rt = threadIdx.x - 384;
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    if constexpr (RED) {
+      // register path: red.global.add.v2 straight from the 16x256b TMEM fragments
+      // (4 threads cover one full 32-byte sector; no smem traffic at all)
+      for (int it = 0; it < n_it; ++it) {
+        mbar_wait(dq_full, it & 1);
+        tc_fence_after();
+        if (rt == 0) HX_BT(9, it);
+        uint32_t v[2][64];
+        tmem_ld_16x256b_x16(tDQ + lane_off, v[0]);
+        tmem_ld_16x256b_x16(tDQ + lane_off + (16u << 16), v[1]);  // (D = 64: columns >= 64 unused)
+        tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(dq_empty);
+        if (rt == 0) HX_BT(10, it);
+        const int q0 = (kt + it) * AT_TILE;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {  // TMEM lanes quad*32 + 16*hh ..
+#pragma unroll
+          for (int rr = 0; rr < 2; ++rr) {
+            const int row = quad * 32 + 16 * hh + (lane >> 2) + 8 * rr;
+            if (q0 + row < p.s) {
+              float* dst = dq_acc + (static_cast<int64_t>(bh) * p.s + q0 + row) * D + 2 * (lane & 3);
+#pragma unroll
+              for (int c = 0; c < 16; ++c)
+                if (8 * c < D) red_add_v2(dst + 8 * c, v[hh][4 * c + 2 * rr], v[hh][4 * c + 2 * rr + 1]);
+            }
+          }
+        }
+        if (rt == 0) HX_BT(11, it);
+      }
+    } else {
+    uint8_t* stg = smem + L::STG;
+      int k = 0;
+      for (int it = 0; it < n_it; ++it) {
+        mbar_wait(dq_full, it & 1);
+        tc_fence_after();
+        if (rt == 0) HX_BT(9, it);
+        uint32_t v[D];
+  #pragma unroll
+        for (int c = 0; c < D / 32; ++c) tmem_ld32(tDQ + lane_off + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
+        tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(dq_empty);
+        if (rt == 0) HX_BT(10, it);
+        const int q0 = (kt + it) * AT_TILE;
+        if (kNoReduce) continue;
+  #pragma unroll
+        for (int c = 0; c < D / 32; ++c, ++k) {
+          uint8_t* buf = stg + (k & 1) * (AT_TILE * 128);
+          if (rt == 0) bulk_wait_read<1>();
+          named_barrier_sync(2, 128);
+  #pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<uint4*>(buf + r * 128 + ((j ^ (r & 7)) << 4)) =
+                make_uint4(v[32 * c + 4 * j], v[32 * c + 4 * j + 1], v[32 * c + 4 * j + 2], v[32 * c + 4 * j + 3]);
+          fence_proxy_async();
+          named_barrier_sync(2, 128);
+          if (rt == 0) {
+            tma_reduce_add_3d(&tm_dq, buf, 32 * c, q0, bh);
+            bulk_commit();
+          }
+        }
+        if (rt == 0) HX_BT(11, it);
+      }
+    }
+    if (rt == 0) bulk_wait_all();
+    finish();
+    return;
+  } else {
+    // compute: thread = key row c, query columns [64g, 64g + 64)
+    regs_inc<136>();
+    const int g = warp >> 2, quad = warp & 3;
+    const int c = quad * 32 + lane;
+    const int qoff = 64 * g;
+    const int ct = threadIdx.x;
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const int64_t row_base = static_cast<int64_t>(bh) * p.s;
+    const int kv_row = kt * AT_TILE + c;
+    uint8_t* sds_row = smem + L::DS + g * (AT_TILE * 128) + c * 128;
+    const uint64_t scale2 = f2pack(p.scale_log2, p.scale_log2);
+    // Statistics of the next query tile: thread ct < 128 loads lse of query ct, the
+    // others delta of query ct-128.  The raw value is only consumed (scaled, negated,
+    // stored to smem) one iteration later, so the global-load latency is hidden.
+    const float* stat_src = (ct < AT_TILE ? p.lse : p.delta) + row_base + (ct & (AT_TILE - 1));
+    const float stat_mul = ct < AT_TILE ? -LOG2E : -1.f;
+    float nxt = 0.f;
+    auto fetch = [&](int it) {
+      const int q = (kt + it) * AT_TILE + (ct & (AT_TILE - 1));
+      nxt = q < p.s ? __ldg(stat_src + (kt + it) * AT_TILE) : 0.f;
+    };
+    fetch(0);
+    for (int it = 0; it < n_it; ++it) {
+      const int q0 = (kt + it) * AT_TILE;
+      float* s_nl = stat + (it & 1) * 2 * AT_TILE;
+      float* s_nd = s_nl + AT_TILE;
+      (ct < AT_TILE ? s_nl : s_nd)[ct & (AT_TILE - 1)] = nxt * stat_mul;
+      named_barrier_sync(1, NT);
+      if (ct == 0) HX_BT(12, it);
+      if (it + 1 < n_it) fetch(it + 1);
+      const bool need_mask = it == 0 || q0 + AT_TILE > p.s;
+      mbar_wait(s_full, it & 1);
+      tc_fence_after();
+      if (ct == 0) HX_BT(5, it);
+      if (ct == 224) HX_BT(14, it);
+      uint32_t raw[64];
+      if (kNoCompute) {
+        tc_fence_before();
+        mbar_arrive(p_full);
+        mbar_wait(dp_full, it & 1);
+        tc_fence_before();
+        mbar_arrive(ds_full);
+        continue;
+      }
+      tmem_ld32(tS + lane_off + qoff, *reinterpret_cast<uint32_t(*)[32]>(raw));
+      tmem_ld32(tS + lane_off + qoff + 32, *reinterpret_cast<uint32_t(*)[32]>(raw + 32));
+      tmem_wait_ld();
+      float pv[64];
+#pragma unroll
+      for (int v = 0; v < 32; ++v) {
+        const float2 l2 = reinterpret_cast<const float2*>(s_nl + qoff)[v];
+        const float2 x = f2unpack(ffma2(f2pack(__uint_as_float(raw[2 * v]), __uint_as_float(raw[2 * v + 1])),
+                                        scale2, f2pack(l2.x, l2.y)));
+        pv[2 * v] = fast_exp2(x.x);
+        pv[2 * v + 1] = fast_exp2(x.y);
+      }
+      if (need_mask) {  // diagonal tile (query < key) and the sequence tail
+#pragma unroll
+        for (int j = 0; j < 64; ++j)
+          if (q0 + qoff + j < kv_row || q0 + qoff + j >= p.s) pv[j] = 0.f;
+      }
+      {
+        uint32_t pk[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) pk[j] = pack_bf16(pv[2 * j], pv[2 * j + 1]);
+        tmem_st32(tS + lane_off + qoff, pk);  // P^T over this warpgroup's S^T columns
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(p_full);
+      if (ct == 0) HX_BT(6, it);
+      mbar_wait(dp_full, it & 1);
+      tc_fence_after();
+      if (ct == 0) HX_BT(7, it);
+      tmem_ld32(tDP + lane_off + qoff, *reinterpret_cast<uint32_t(*)[32]>(raw));
+      tmem_ld32(tDP + lane_off + qoff + 32, *reinterpret_cast<uint32_t(*)[32]>(raw + 32));
+      tmem_wait_ld();
+      {
+        uint32_t pk[32];
+#pragma unroll
+        for (int v = 0; v < 32; ++v) {
+          const float2 d2 = reinterpret_cast<const float2*>(s_nd + qoff)[v];
+          const float2 ds = f2unpack(fmul2(fadd2(f2pack(__uint_as_float(raw[2 * v]), __uint_as_float(raw[2 * v + 1])),
+                                                 f2pack(d2.x, d2.y)),
+                                           f2pack(pv[2 * v], pv[2 * v + 1])));
+          pk[v] = pack_bf16(ds.x, ds.y);
+        }
+        tmem_st32(tDP + lane_off + qoff, pk);  // dS^T over this warpgroup's dP^T columns
+#pragma unroll
+        for (int j = 0; j < 8; ++j)  // dS^T row c, query columns 64g + 8j.. (SW128 atom g)
+          *reinterpret_cast<uint4*>(sds_row + ((j ^ (c & 7)) << 4)) =
+              make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+      }
+      fence_proxy_async();
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(ds_full);
+      if (ct == 0) HX_BT(8, it);
+      if (ct == 224) HX_BT(13, it);
+    }
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    const int64_t kv_tok = static_cast<int64_t>(kv_row) * p.b + bi;
+    __nv_bfloat16* dst = p.dqkv + kv_tok * p.ld_dqkv + head * D;
+    acc_row_out<D, 2>(tDK + lane_off, g, dst + p.h, p.scale, kv_row < p.s);
+    acc_row_out<D, 2>(tDV + lane_off, g, dst + 2 * p.h, 1.f, kv_row < p.s);
+    finish();
+  }
+}
+
+// dq (bf16, into dqkv's q columns) = scale * fp32 accumulator [b*heads][s][D].
+template <int D>
+__global__ void __launch_bounds__(256) attn_bwd_dq_convert_kernel(const float* __restrict__ acc, AttnParams p) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;  // 8 columns each
+  constexpr int VPR = D / 8;
+  const int64_t total = static_cast<int64_t>(p.b) * p.heads * p.s * VPR;
+  if (idx >= total) return;
+  const int v = static_cast<int>(idx % VPR);
+  const int64_t row = idx / VPR;  // (bh, q)
+  const int q = static_cast<int>(row % p.s);
+  const int bh = static_cast<int>(row / p.s);
+  const int bi = bh / p.heads, head = bh % p.heads;
+  const float4 a = reinterpret_cast<const float4*>(acc + row * D)[2 * v];
+  const float4 b = reinterpret_cast<const float4*>(acc + row * D)[2 * v + 1];
+  const float sc = p.scale;
+  const uint4 o = make_uint4(pack_bf16(a.x * sc, a.y * sc), pack_bf16(a.z * sc, a.w * sc), pack_bf16(b.x * sc, b.y * sc),
+                             pack_bf16(b.z * sc, b.w * sc));
+  *reinterpret_cast<uint4*>(p.dqkv + (static_cast<int64_t>(q) * p.b + bi) * p.ld_dqkv + head * D + 8 * v) = o;
+}
+
 // ------------------------------------------------------------------ pre-pass
 
 // D = rowsum(dO * O) per (batch, head, query): one warp per token.
@@ -882,8 +1290,47 @@ static cudaError_t bwd9_launch(const void* qkv, int ld_qkv, const void* o, const
   return cudaGetLastError();
 }
 
+template <int D>
+static cudaError_t fused_launch(const void* qkv, int ld_qkv, const void* o, const void* d_o, int ld_o, float* dq_acc,
+                                const AttnParams& p, cudaStream_t st) {
+  CUtensorMap tq, tdo, tdq;
+  cudaError_t e = make_tma_3d_rows(&tq, qkv, 3 * p.h, p.b, p.s, ld_qkv, 64, AT_TILE);
+  if (e == cudaSuccess) e = make_tma_3d_rows(&tdo, d_o, p.h, p.b, p.s, ld_o, 64, AT_TILE);
+  if (e == cudaSuccess) e = make_tma_f32_3d(&tdq, dq_acc, D, p.s, static_cast<uint64_t>(p.b) * p.heads, 32, AT_TILE);
+  if (e != cudaSuccess) return e;
+  // dQ reduction path: TMA bulk reduce-add through smem staging (default) or
+  // red.global from registers (HX_DQ_RED=1), for A/B runs.
+  static const bool red = getenv("HX_DQ_RED") && atoi(getenv("HX_DQ_RED")) != 0;
+  static bool cfg = false;
+  if (!cfg) {
+    e = cudaFuncSetAttribute(attn_bwd_fused_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             FusedSmem<D>::TOTAL);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(attn_bwd_fused_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               FusedSmem<D>::TOTAL);
+    if (e != cudaSuccess) return e;
+    cfg = true;
+  }
+  const int tokens = p.s * p.b;
+  e = cudaMemsetAsync(dq_acc, 0, static_cast<size_t>(tokens) * p.h * sizeof(float), st);
+  if (e != cudaSuccess) return e;
+  attn_bwd_pre_kernel<D><<<(tokens + 7) / 8, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(o),
+                                                           static_cast<const __nv_bfloat16*>(d_o), ld_o,
+                                                           const_cast<float*>(p.delta), p.s, p.b, p.heads);
+  dim3 grid((p.s + AT_TILE - 1) / AT_TILE, p.b * p.heads);
+  if (red)
+    attn_bwd_fused_kernel<D, true><<<grid, 512, FusedSmem<D>::TOTAL, st>>>(tq, tdo, tdq, dq_acc, p);
+  else
+    attn_bwd_fused_kernel<D, false><<<grid, 512, FusedSmem<D>::TOTAL, st>>>(tq, tdo, tdq, dq_acc, p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int64_t vecs = static_cast<int64_t>(tokens) * p.h / 8;
+  attn_bwd_dq_convert_kernel<D><<<static_cast<unsigned>((vecs + 255) / 256), 256, 0, st>>>(dq_acc, p);
+  return cudaGetLastError();
+}
+
 cudaError_t attn_bwd_launch(const void* qkv, int ld_qkv, const void* o, const void* d_o, int ld_o,
-                            const float* lse, float* delta, float* /*dq_ws: unused, atomic-free*/, void* dqkv,
+                            const float* lse, float* delta, float* dq_acc, void* dqkv,
                             int ld_dqkv, int s, int b, int heads, int d, cudaStream_t st) {
   AttnParams p{};
   p.s = s;
@@ -896,9 +1343,14 @@ cudaError_t attn_bwd_launch(const void* qkv, int ld_qkv, const void* o, const vo
   p.delta = delta;
   p.dqkv = static_cast<__nv_bfloat16*>(dqkv);
   p.ld_dqkv = ld_dqkv;
-  // Default: the 128-wide v9 kernels.  HX_ATTN_BWD=8 selects the 64-wide kernels
-  // (HX_ATTN_NWG=2|4 compute warpgroups) for A/B runs.
-  static const int variant = getenv("HX_ATTN_BWD") ? atoi(getenv("HX_ATTN_BWD")) : 9;
+  // Default: the fused one-pass kernel (v10).  HX_ATTN_BWD=9 selects the split
+  // atomic-free dK/dV + dQ kernels, 8 the 64-wide split kernels, for A/B runs.
+  static const int variant = getenv("HX_ATTN_BWD") ? atoi(getenv("HX_ATTN_BWD")) : 10;
+  if (variant == 10) {
+    if (d == 128) return fused_launch<128>(qkv, ld_qkv, o, d_o, ld_o, dq_acc, p, st);
+    if (d == 64) return fused_launch<64>(qkv, ld_qkv, o, d_o, ld_o, dq_acc, p, st);
+    return cudaErrorNotSupported;
+  }
   if (variant == 9) {
     if (d == 128) return bwd9_launch<128>(qkv, ld_qkv, o, d_o, ld_o, p, st);
     if (d == 64) return bwd9_launch<64>(qkv, ld_qkv, o, d_o, ld_o, p, st);
@@ -913,3 +1365,9 @@ cudaError_t attn_bwd_launch(const void* qkv, int ld_qkv, const void* o, const vo
 }
 
 }  // namespace hx
+
+#ifdef HX_BWD_TRACE
+extern "C" HX_API int hx_debug_bwd_trace(long long* out) {
+  return static_cast<int>(cudaMemcpyFromSymbol(out, hx::g_bwd_trace, sizeof(hx::g_bwd_trace)));
+}
+#endif

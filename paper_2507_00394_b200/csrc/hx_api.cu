@@ -44,11 +44,12 @@ static EncodeTiled encode_fn() {
 }
 
 static cudaError_t encode(CUtensorMap* map, const void* ptr, cuuint32_t rank, const cuuint64_t* dims,
-                          const cuuint64_t* strides, const cuuint32_t* box) {
+                          const cuuint64_t* strides, const cuuint32_t* box,
+                          CUtensorMapDataType dtype = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16) {
   EncodeTiled fn = encode_fn();
   if (!fn) return cudaErrorInitializationError;
   cuuint32_t elem_strides[3] = {1, 1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), dims, strides, box,
+  CUresult r = fn(map, dtype, rank, const_cast<void*>(ptr), dims, strides, box,
                   elem_strides, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
@@ -68,6 +69,14 @@ cudaError_t make_tma_3d_rows(CUtensorMap* map, const void* ptr, uint64_t cols, u
   const cuuint64_t strides[2] = {ld * 2, ld * b * 2};
   const cuuint32_t box[3] = {box_cols, 1, box_rows};
   return encode(map, ptr, 3, dims, strides, box);
+}
+
+cudaError_t make_tma_f32_3d(CUtensorMap* map, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2,
+                            uint32_t box0, uint32_t box1) {
+  const cuuint64_t dims[3] = {d0, d1, d2};
+  const cuuint64_t strides[2] = {d0 * 4, d0 * d1 * 4};
+  const cuuint32_t box[3] = {box0, box1, 1};
+  return encode(map, ptr, 3, dims, strides, box, CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
 }
 
 }  // namespace hx

@@ -36,6 +36,11 @@ cudaError_t make_tma_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64
 cudaError_t make_tma_3d_rows(CUtensorMap* map, const void* ptr, uint64_t cols, uint64_t b, uint64_t s,
                              uint64_t ld, uint32_t box_cols, uint32_t box_rows);
 
+// 3-D fp32 tensor map over a dense [d2][d1][d0] array, SWIZZLE_128B, box
+// {box0, box1, 1} (box0 * 4 bytes must be 128).  Used for TMA reduce-adds.
+cudaError_t make_tma_f32_3d(CUtensorMap* map, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2,
+                            uint32_t box0, uint32_t box1);
+
 cudaError_t ln_fwd_launch(const void* x, const float* g, const float* b, void* y, int rows, int h,
                           cudaStream_t st);
 cudaError_t ln_bwd_launch(const void* dy, const void* x, const float* g, const void* dres, void* dx,

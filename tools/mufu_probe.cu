@@ -54,6 +54,52 @@ __global__ void k_ffma(float* out, float seed) {
   if (s == 12345.f) out[0] = s;
 }
 
+__device__ __forceinline__ uint32_t cvt_bf16x2(float lo, float hi) {
+  uint32_t r;
+  asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+// bf16x2 by integer round-half-up and a byte permute (ALU pipe only)
+__device__ __forceinline__ uint32_t alu_bf16x2(float lo, float hi) {
+  const uint32_t a = __float_as_uint(lo) + 0x8000u, b = __float_as_uint(hi) + 0x8000u;
+  uint32_t r;
+  asm volatile("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+
+// one F2FP per inner op (LOP3 feeds the next input)
+__global__ void k_f2fp(float* out, float seed) {
+  float v[CH];
+  for (int c = 0; c < CH; ++c) v[c] = seed * (threadIdx.x + c);
+  for (int i = 0; i < ITERS; ++i)
+#pragma unroll
+    for (int c = 0; c < CH; ++c) v[c] = __uint_as_float(cvt_bf16x2(v[c], v[c]) ^ 0x1u);
+  float s = 0;
+  for (int c = 0; c < CH; ++c) s += v[c];
+  if (s == 12345.f) out[0] = s;
+}
+__global__ void k_alupack(float* out, float seed) {
+  float v[CH];
+  for (int c = 0; c < CH; ++c) v[c] = seed * (threadIdx.x + c);
+  for (int i = 0; i < ITERS; ++i)
+#pragma unroll
+    for (int c = 0; c < CH; ++c) v[c] = __uint_as_float(alu_bf16x2(v[c], v[c]) ^ 0x1u);
+  float s = 0;
+  for (int c = 0; c < CH; ++c) s += v[c];
+  if (s == 12345.f) out[0] = s;
+}
+// one EX2 + one F2FP per inner op: if they share the XU pipe this takes ~2x k_ex2
+__global__ void k_ex2_f2fp(float* out, float seed) {
+  float v[CH];
+  for (int c = 0; c < CH; ++c) v[c] = seed * (threadIdx.x + c) * 1e-9f;
+  for (int i = 0; i < ITERS; ++i)
+#pragma unroll
+    for (int c = 0; c < CH; ++c) v[c] = __uint_as_float(cvt_bf16x2(ex2(v[c]), v[c]) & 0x3fff3fffu);
+  float s = 0;
+  for (int c = 0; c < CH; ++c) s += v[c];
+  if (s == 12345.f) out[0] = s;
+}
+
 int main() {
   int dev = 0, sms = 0, clk = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -81,6 +127,9 @@ int main() {
   run("mufu_ex2", k_ex2, 1.0);
   run("ffma2_lanes", k_ffma2, 2.0);
   run("ffma", k_ffma, 1.0);
+  run("f2fp_bf16x2", k_f2fp, 1.0);
+  run("alu_bf16x2", k_alupack, 1.0);
+  run("ex2+f2fp (pairs)", k_ex2_f2fp, 1.0);
   printf("{\"sms\": %d, \"max_clock_mhz\": %d, \"err\": \"%s\"}\n", sms, clk / 1000,
          cudaGetErrorString(cudaGetLastError()));
   return 0;

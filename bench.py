@@ -55,6 +55,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-s", type=int, default=256)
+    ap.add_argument("--stash-budget-gb", type=float, default=None,
+                    help="device budget for stashed activations; the rest is FILO-offloaded to pinned "
+                         "host memory ('auto': free HBM after weights/grads minus a working-set margin; "
+                         "default: auto for gpt7b_128k, off otherwise)")
     ap.add_argument("--compare-1f1b", choices=["auto", "yes", "no"], default="auto",
                     help="also time the same-kernel 1F1B schedule (default: only when N > 1)")
     return ap.parse_args()
@@ -219,6 +223,9 @@ def main() -> None:
     if world > 1:
         # leave SMs for the NCCL p2p kernels that run next to persistent GEMMs
         os.environ.setdefault("HX_SM_RESERVE", "8")
+    if args.workload == "gpt7b_128k" or args.stash_budget_gb is not None:
+        # offloading churns GB-sized blocks: grow segments instead of fragmenting them
+        os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
 
     import torch
     import torch.distributed as dist
@@ -258,9 +265,19 @@ def main() -> None:
                 layers[l] = DeviceLayer({k: v for k, v in full.items() if k in need},
                                         tuple(k for k in full if k in own))
             del full
+        budget = None
+        if args.stash_budget_gb is not None and args.stash_budget_gb >= 0:
+            budget = int(args.stash_budget_gb * 2**30)
+        elif args.stash_budget_gb is not None or args.workload == "gpt7b_128k":
+            # free HBM after weights + fp32 grads, minus the per-task working set
+            # (regenerated post stash, MLP gradients, qkv / dqkv, attention workspaces:
+            # ~22 x T*h bf16 at the last layer's backward) and allocator slack
+            torch.cuda.synchronize()
+            free, _total = torch.cuda.mem_get_info(dev)
+            budget = max(0, free - 40 * cfg.s * cfg.b * cfg.h * 2)
         return HelixRuntime(schedule, DeviceModel(layers), args.mlp_chunk,
                             "distributed" if world > 1 else "replay", dev,
-                            rank=rank if world > 1 else None, groups=groups)
+                            rank=rank if world > 1 else None, groups=groups, stash_budget_bytes=budget)
 
     rt = build_runtime(sched)
     T = cfg.s * cfg.b
@@ -439,6 +456,7 @@ def main() -> None:
             "cpu_baseline": cpu,
             "clocks": clk,
             "max_memory_gb": torch.cuda.max_memory_allocated(dev) / 2**30,
+            "stash_offload": rt.offload_stats(),
         }
         print(json.dumps(line), flush=True)
     if world > 1:

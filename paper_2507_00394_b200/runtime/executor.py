@@ -64,6 +64,7 @@ class RunResult:
     peak_stash_elements: list[int]
     mode: str
     timeline: dict[str, tuple[float, float]] | None = None   # device ms, if recorded
+    offload: dict | None = None    # host-offload statistics, when a stash budget was set
 
 
 # Stash entries that exist only for the flash backward (never part of the
@@ -72,7 +73,7 @@ _LOCAL_EXTRAS = ("o", "lse")
 
 
 def _logical_elements(entry: dict) -> int:
-    return sum(int(t.numel()) for k, t in entry.items() if k not in _LOCAL_EXTRAS)
+    return sum(int(t.numel()) for k, t in entry.items() if k not in _LOCAL_EXTRAS)  # tensors or offloaded placeholders
 
 
 class _Stage:
@@ -153,6 +154,7 @@ class _Core:
         self.math = math
         self.stages = stages
         self.sumsq = sumsq
+        self.offload = None   # StashOffloader (FILO host offload) or None
         self.inputs: list[torch.Tensor] = []
         self.recv_of_send = {t.deps[0]: t.id for t in self.tasks.values() if t.kind == RECV}
         self.sends_by_producer: dict[str, list[Task]] = {}
@@ -194,6 +196,8 @@ class _Core:
 
     def store_stash(self, st: _Stage, l: int, mb: int, comp: str, full: dict, payload: dict) -> None:
         st.stash[(l, mb, comp)] = self.math.reduce_stash(comp, full, payload) if self.rc else full
+        if self.offload is not None:
+            self.offload.after_store(st, (l, mb, comp))
 
     def W(self, l: int):
         return self.model.layers[l].w
@@ -205,6 +209,14 @@ class _Core:
 
     def run_compute(self, t: Task) -> None:
         st = self.stages[t.stage]
+        if self.offload is not None:
+            self.offload.before_task(st, t)
+        self._run_compute(st, t)
+        if self.offload is not None:
+            self.offload.after_task(st, t)
+        st.bump()
+
+    def _run_compute(self, st: _Stage, t: Task) -> None:
         if t.kind == FWD:
             (self._fwd_chunk if t.comp == "chunk" else self._fwd_component)(st, t)
         elif t.kind == BWD_B:
@@ -219,7 +231,6 @@ class _Core:
                                                        self.W(t.layer) if t.layer in self.model.layers else None)
         else:
             raise ExecutionError(f"{t.id}: kind {t.kind} is not a compute task")
-        st.bump()
 
     def _loss(self, z: torch.Tensor, mb: int) -> torch.Tensor:
         return self.math.loss(z, self.sumsq[mb:mb + 1])
@@ -618,7 +629,8 @@ class HelixRuntime:
 
     def __init__(self, sched: Schedule, model: DeviceModel, mlp_chunk: int | None = None,
                  mode: str = "replay", device=None, math=None, rank: int | None = None,
-                 groups: dict | None = None, record_timeline: bool = False):
+                 groups: dict | None = None, record_timeline: bool = False,
+                 stash_budget_bytes: int | None = None, offload_min_bytes: int = 32 << 20):
         self.sched = sched
         self.cfg = meta_config(sched)
         self.mode = mode
@@ -635,12 +647,19 @@ class HelixRuntime:
         self.groups = groups
         self.record_timeline = record_timeline
         self.timeline = None
+        if stash_budget_bytes is not None:
+            from .offload import StashOffloader
+            weights = [w for dl in model.layers.values() for w in dl.w.values()]
+            self.core.offload = StashOffloader(sched, self.stages, weights, stash_budget_bytes,
+                                               min_bytes=offload_min_bytes)
 
     def run(self, inputs: list[torch.Tensor]) -> None:
         cfg = self.cfg
         if len(inputs) != cfg.m:
             raise ExecutionError(f"need {cfg.m} input microbatches, got {len(inputs)}")
         self.core.inputs = [x.reshape(cfg.s * cfg.b, cfg.h) for x in inputs]
+        if self.core.offload is not None:
+            self.core.offload.exclude(self.core.inputs)
         for st in self.stages.values():
             st.peak = 0
         self.model.zero_grads(self.math.zero_)
@@ -665,6 +684,13 @@ class HelixRuntime:
         dirty = [st.idx for st in self.stages.values() if st.stash or st.wctx]
         if dirty:
             raise ExecutionError(f"stash not drained on stages {dirty}")
+
+    def offload_stats(self) -> dict | None:
+        off = self.core.offload
+        if off is None:
+            return None
+        live = sum(len(e) for e in off.entries.values())
+        return {**off.stats, "budget_bytes": off.budget, "live_entries": live}
 
     def loss_stage(self, mb: int) -> int:
         chunked = any(t.comp == "chunk" for t in self.sched.tasks.values() if t.is_compute)
@@ -692,13 +718,19 @@ def _to_device_inputs(inputs, cfg, device) -> list[torch.Tensor]:
 
 def execute_schedule(sched: Schedule, params: list[LayerParams], inputs: list,
                      mlp_chunk: int | None = None, threaded: bool = False,
-                     record_timeline: bool = False) -> RunResult:
+                     record_timeline: bool = False, *, stash_budget_bytes: int | None = None,
+                     offload_min_bytes: int = 32 << 20) -> RunResult:
     """Run ``sched`` numerically on the B200(s); same contract as the reference.
 
     ``threaded=False``: replay on the current GPU.  ``threaded=True``: one rank
     per stage when ``torch.distributed`` is initialised with world size ==
     n_stages (every rank calls this and gets the same, all-gathered result),
     otherwise one CUDA stream per stage on the current GPU.
+
+    ``stash_budget_bytes`` (B200 extension): keep at most this many bytes of
+    stashed activations per process on the device, FILO-offloading the rest to
+    pinned host memory (``runtime/offload.py``); tensors smaller than
+    ``offload_min_bytes`` always stay.
     """
     cfg = meta_config(sched)
     if len(params) != cfg.L:
@@ -714,11 +746,13 @@ def execute_schedule(sched: Schedule, params: list[LayerParams], inputs: list,
         rank = torch.distributed.get_rank()
         model = DeviceModel.from_host(sched, params, [rank], device)
         rt = HelixRuntime(sched, model, mlp_chunk, "distributed", device, rank=rank,
-                          groups=make_pair_groups(sched.n_stages), record_timeline=record_timeline)
+                          groups=make_pair_groups(sched.n_stages), record_timeline=record_timeline,
+                          stash_budget_bytes=stash_budget_bytes, offload_min_bytes=offload_min_bytes)
     else:
         model = DeviceModel.from_host(sched, params, range(sched.n_stages), device)
         rt = HelixRuntime(sched, model, mlp_chunk, "multistream" if threaded else "replay", device,
-                          record_timeline=record_timeline)
+                          record_timeline=record_timeline, stash_budget_bytes=stash_budget_bytes,
+                          offload_min_bytes=offload_min_bytes)
     rt.run(_to_device_inputs(inputs, cfg, device))
     torch.cuda.synchronize()
     if dist:
@@ -727,7 +761,7 @@ def execute_schedule(sched: Schedule, params: list[LayerParams], inputs: list,
     losses = rt.losses()
     peaks = [rt.stages[i].peak for i in range(sched.n_stages)]
     return RunResult(losses, [grads[l] for l in range(cfg.L)], peaks, "threaded" if threaded else "replay",
-                     rt.timeline)
+                     rt.timeline, rt.offload_stats())
 
 
 def _gather_distributed(rt: HelixRuntime, params) -> RunResult:

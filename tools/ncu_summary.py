@@ -29,6 +29,9 @@ KEYS = {
     "sm_throughput_pct": ("sm__throughput.avg.pct_of_peak_sustained_elapsed", 1),
     "dram_throughput_pct": ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", 1),
     "warps_active_pct": ("sm__warps_active.avg.pct_of_peak_sustained_active", 1),
+    "l2_throughput_pct": ("lts__throughput.avg.pct_of_peak_sustained_elapsed", 1),
+    "l2_reduce_input_pct": ("lts__d_atomic_input_cycles_active.avg.pct_of_peak_sustained_elapsed", 1),
+    "xu_pipe_pct": ("sm__inst_executed_pipe_xu_realtime.avg.pct_of_peak_sustained_elapsed", 1),
 }
 UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1, "us": 1e3, "ms": 1e6,
               "usecond": 1e3, "msecond": 1e6, "nsecond": 1}
@@ -47,6 +50,8 @@ def summarize(rep: Path) -> dict:
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     col = {h: i for i, h in enumerate(hdr)}
+    for h, i in list(col.items()):  # section-prefixed names (e.g. "TPC.TriageCompute.<metric>")
+        col.setdefault(h.split(".", 2)[-1] if h.count(".") >= 3 and h.split(".")[0].isupper() else h, i)
     out = {}
     for r in rows[2:]:
         name = short(r[col["Kernel Name"]])
@@ -98,7 +103,7 @@ def main():
             rec["tag"] = args.tag
             data[name] = rec
             # convenient aliases for bench.py's roofline 'traffic'
-            if name.startswith("attn_bwd_kernel"):
+            if name.startswith("attn_bwd_fused_kernel"):
                 data["attn_bwd"] = rec
             if name.startswith("attn_fwd_kernel"):
                 data["attn_fwd"] = rec

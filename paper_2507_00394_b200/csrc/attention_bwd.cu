@@ -857,8 +857,10 @@ __global__ void __launch_bounds__(512, 1)
   uint64_t* dq_full = bars + 11;
   uint64_t* dq_empty = bars + 12; // 128 arrivals
   uint64_t* acc_full = bars + 13;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
-  constexpr int NBARS = 14;
+  [[maybe_unused]] uint64_t* dv_done = bars + 14;  // trace builds only: completion of dV / dK groups
+  [[maybe_unused]] uint64_t* dk_done = bars + 15;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  constexpr int NBARS = 16;
   float* stat = reinterpret_cast<float*>(smem + L::STAT);
 
   const int warp = warp_id(), lane = lane_id();
@@ -909,7 +911,26 @@ __global__ void __launch_bounds__(512, 1)
         mbar_arrive_expect_tx(do_full, Tile<D>::BYTES);
         tma_tile_rows<D>(smem + L::DO, &tm_do, do_full, head * D, bi, q0, AT_TILE);
       }
-    } else if (warp == 9) {
+    }
+#ifdef HX_BWD_TRACE
+    else if (warp == 10 && lane == 0) {  // observer: completion time of every MMA group
+      for (int it = 0; it < n_it; ++it) {
+        mbar_wait(dp_full, it & 1);
+        HX_BT(16, it);
+        mbar_wait(dv_done, it & 1);
+        HX_BT(17, it);
+        if (it + 1 < n_it) {
+          mbar_wait(s_full, (it + 1) & 1);
+          HX_BT(18, it);
+        }
+        mbar_wait(dk_done, it & 1);
+        HX_BT(19, it);
+        mbar_wait(dq_full, it & 1);
+        HX_BT(20, it);
+      }
+    }
+#endif
+    else if (warp == 9) {
       // The whole warp runs the issue loop (warp-uniform descriptors on the uniform
       // datapath); one elected lane issues each tcgen05 instruction.  Fully unrolled
       // chains: the tensor pipe's queue is shallow, so per-MMA issue cost must stay
@@ -960,6 +981,9 @@ __global__ void __launch_bounds__(512, 1)
         tc_fence_after();
         HX_BT(0, it);
         mma_ts_mn(tDV, tS, sdo, id_kv, it > 0);
+#ifdef HX_BWD_TRACE
+        umma_commit_e(dv_done);
+#endif
         umma_commit_e(do_empty);  // dO(it) read by dP^T(it) and dV(it)
         if (it + 1 < n_it) issue_s(it + 1);
         HX_BT(2, it);
@@ -967,6 +991,9 @@ __global__ void __launch_bounds__(512, 1)
         tc_fence_after();
         HX_BT(3, it);
         mma_ts_mn(tDK, tDP, sq(it), id_kv, it > 0);
+#ifdef HX_BWD_TRACE
+        umma_commit_e(dk_done);
+#endif
         umma_commit_e(&q_empty[it & 1]);
         if (!DQ_SHARES_DP && it > 0) {
           mbar_wait(dq_empty, (it - 1) & 1);
@@ -1161,6 +1188,7 @@ __global__ void __launch_bounds__(512, 1)
       tc_fence_before();
       mbar_arrive(ds_full);
       if (ct == 0) HX_BT(8, it);
+      if (ct == 224) HX_BT(13, it);
       if (ct == 224) HX_BT(13, it);
     }
     mbar_wait(acc_full, 0);

@@ -116,7 +116,12 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row, int
   }
 }
 
-template <int BN, bool A_MN, bool B_MN>
+// CL = true: clusters of 2 CTAs on vertically adjacent M-blocks that share the
+// B panel.  Each CTA TMA-loads its own A tile and HALF of the B tile, multicast
+// to both CTAs, so L2->SM traffic per MMA drops from (A + B) to (A + B/2): 48 ->
+// 32 KB per 64-deep stage at BN = 256.  A stage is refilled only after both
+// CTAs' MMAs released it (multicast commits on a count-2 empty barrier).
+template <int BN, bool A_MN, bool B_MN, bool CL>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tm_a,
                       const __grid_constant__ CUtensorMap tm_b, const GemmParams p) {
@@ -133,15 +138,24 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int lane = lane_id();
   const int num_m = (p.M + GEMM_BM - 1) / GEMM_BM;
   const int num_n = (p.N + BN - 1) / BN;
-  const int num_tiles = num_m * num_n;
   const int num_k = (p.K + GEMM_BK - 1) / GEMM_BK;
+  // persistent walk over (cluster) tiles: with CL a tile is an M-block pair
+  const int rank = CL ? static_cast<int>(cluster_ctarank()) : 0;
+  const int num_m_w = CL ? num_m / 2 : num_m;
+  const int num_tiles = num_m_w * num_n;
+  const int first = CL ? static_cast<int>(cluster_id_x()) : static_cast<int>(blockIdx.x);
+  const int stride = CL ? static_cast<int>(nclusters_x()) : static_cast<int>(gridDim.x);
+  auto coords = [&](int t, int& mb, int& nb) {
+    tile_coords(t, num_m_w, num_n, mb, nb);
+    if (CL) mb = 2 * mb + rank;
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm_a);
     tma_prefetch(&tm_b);
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CL ? 2 : 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -152,6 +166,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (warp == 2) tmem_alloc(tmem_slot, C::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
+  if (CL) cluster_sync();  // peers' barriers initialised before any multicast lands
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -160,9 +175,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       // ---------------- TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int t = first; t < num_tiles; t += stride) {
         int mb, nb;
-        tile_coords(t, num_m, num_n, mb, nb);
+        coords(t, mb, nb);
         const int m0 = mb * GEMM_BM, n0 = nb * BN;
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -176,7 +191,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           } else {
             tma_load_2d(sa, &tm_a, &full[stage], k0, m0);
           }
-          if (B_MN) {
+          if (CL) {  // this CTA's half of B, multicast to both CTAs of the pair
+            if (B_MN) {
+#pragma unroll
+              for (int j = rank * (BN / 128); j < (rank + 1) * (BN / 128); ++j)
+                tma_load_2d_mc(sb + j * 8192, &tm_b, &full[stage], n0 + 64 * j, k0, 0x3);
+            } else {
+              tma_load_2d_mc(sb + rank * (BN / 2) * 128, &tm_b, &full[stage], k0, n0 + rank * (BN / 2), 0x3);
+            }
+          } else if (B_MN) {
 #pragma unroll
             for (int j = 0; j < BN / 64; ++j)
               tma_load_2d(sb + j * 8192, &tm_b, &full[stage], n0 + 64 * j, k0);
@@ -194,7 +217,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      for (int t = first; t < num_tiles; t += stride, ++it) {
         const int acc = it & 1;
         mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -212,7 +235,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                                      : sw128_desc(sb + kk * 32, 16, 1024);
             umma_f16_ss(d_tmem, da, db, idesc, (kb | kk) != 0);
           }
-          umma_commit(&empty[stage]);
+          if (CL)
+            umma_commit_mc(&empty[stage], 0x3);  // the stage holds both CTAs' B halves
+          else
+            umma_commit(&empty[stage]);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
         umma_commit(&tfull[acc]);
@@ -222,9 +248,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // ---------------- epilogue
     const int sub = warp & 3;  // TMEM lane quadrant this warp may access
     int it = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+    for (int t = first; t < num_tiles; t += stride, ++it) {
       int mb, nb;
-      tile_coords(t, num_m, num_n, mb, nb);
+      coords(t, mb, nb);
       const int acc = it & 1;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
@@ -244,6 +270,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   }
   __syncthreads();
+  if (CL) cluster_sync();  // no CTA leaves while its peer may still multicast into it
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, C::TMEM_COLS);
@@ -252,21 +279,38 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
 // ------------------------------------------------------------------ host side
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, bool CL>
 static cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
                                int num_sms, cudaStream_t stream) {
   using C = GemmCfg<BN>;
-  auto kern = gemm_sm100_kernel<BN, A_MN, B_MN>;
+  auto kern = gemm_sm100_kernel<BN, A_MN, B_MN, CL>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+    if (e == cudaSuccess && CL) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
     configured = true;
   }
   const int tiles = ((p.M + GEMM_BM - 1) / GEMM_BM) * ((p.N + BN - 1) / BN);
-  const int grid = tiles < num_sms ? tiles : num_sms;
-  kern<<<grid, GEMM_THREADS, C::SMEM_BYTES, stream>>>(ta, tb, p);
-  return cudaGetLastError();
+  int grid = tiles < num_sms ? tiles : num_sms;
+  if (!CL) {
+    kern<<<grid, GEMM_THREADS, C::SMEM_BYTES, stream>>>(ta, tb, p);
+    return cudaGetLastError();
+  }
+  grid &= ~1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.dynamicSmemBytes = C::SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, ta, tb, p);
 }
 
 static int pick_bn(int M, int N, int num_sms) {
@@ -294,12 +338,19 @@ cudaError_t gemm_launch(const GemmOperand& a, const GemmOperand& b, const GemmPa
   cudaError_t e = a.mn ? make_tma_2d(&ta, a.ptr, p.K, p.M, a.ld, 64, 64)
                        : make_tma_2d(&ta, a.ptr, p.M, p.K, a.ld, 64, GEMM_BM);
   if (e != cudaSuccess) return e;
+  // 2-CTA clusters with B multicast when the M-blocks pair up evenly and there are
+  // enough tile pairs to fill the machine (HX_GEMM_CLUSTER=0 disables, for A/B runs)
+  static const bool allow_cl = !getenv("HX_GEMM_CLUSTER") || atoi(getenv("HX_GEMM_CLUSTER")) != 0;
+  const int num_m = (p.M + GEMM_BM - 1) / GEMM_BM;
+  const bool cl = allow_cl && bn == 256 && num_m % 2 == 0 &&
+                  (num_m / 2) * ((p.N + bn - 1) / bn) >= num_sms / 2;
   e = b.mn ? make_tma_2d(&tb, b.ptr, p.K, p.N, b.ld, 64, 64)
-           : make_tma_2d(&tb, b.ptr, p.N, p.K, b.ld, 64, bn);
+           : make_tma_2d(&tb, b.ptr, p.N, p.K, b.ld, 64, cl ? bn / 2 : bn);
   if (e != cudaSuccess) return e;
-#define HX_GEMM_CASE(BN_, AM_, BM_)                                        \
-  if (bn == BN_ && a.mn == AM_ && b.mn == BM_)                               \
-    return launch_gemm<BN_, AM_, BM_>(ta, tb, p, num_sms, stream);
+#define HX_GEMM_CASE(BN_, AM_, BM_)                                                   \
+  if (bn == BN_ && a.mn == AM_ && b.mn == BM_)                                          \
+    return cl ? launch_gemm<BN_, AM_, BM_, true>(ta, tb, p, num_sms, stream)             \
+              : launch_gemm<BN_, AM_, BM_, false>(ta, tb, p, num_sms, stream);
   HX_GEMM_CASE(256, false, true)
   HX_GEMM_CASE(256, false, false)
   HX_GEMM_CASE(256, true, true)

@@ -26,7 +26,9 @@ def rnd(*shape, scale=1.0, seed=0):
     return (torch.randn(*shape, generator=g, device=DEV) * scale).to(torch.bfloat16)
 
 
-GEMM_SHAPES = [(256, 256, 256), (1024, 768, 256), (304, 200, 72), (128, 2048, 512), (2048, 1024, 1024)]
+GEMM_SHAPES = [(256, 256, 256), (1024, 768, 256), (304, 200, 72), (128, 2048, 512), (2048, 1024, 1024),
+               # enough 256x256 M-block pairs for the 2-CTA multicast path (incl. ragged edges)
+               (4096, 2560, 512), (4000, 2504, 200)]
 
 
 @pytest.mark.parametrize("M,N,Kd", GEMM_SHAPES)

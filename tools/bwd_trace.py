@@ -21,7 +21,8 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
 EVENTS = ["mma_dV", "mma_dP", "mma_S_next", "mma_dK", "mma_dQ", "c_s_seen", "c_p_done", "c_dp_seen",
-          "c_ds_done", "r_dq_seen", "r_dq_free", "r_stage_done", "c_bar_passed", "c7_ds_done", "c7_s_seen", "unused"]
+          "c_ds_done", "r_dq_seen", "r_dq_free", "r_stage_done", "c_bar_passed", "c7_ds_done", "c7_s_seen", "unused",
+          "done_dP", "done_dV", "done_S_next", "done_dK", "done_dQ", "u21", "u22", "u23"]
 
 
 def build() -> Path:
@@ -61,7 +62,7 @@ def main():
         K.attention_bwd(qkv, o, do, lse, s, 1, heads, dqkv, delta, dq)
     torch.cuda.synchronize()
     cl = ctypes.CDLL(str(lib))
-    buf = (ctypes.c_longlong * (16 * 512))()
+    buf = (ctypes.c_longlong * (24 * 512))()
     assert cl.hx_debug_bwd_trace(buf) == 0
     tr = {e: list(buf[i * 512:(i + 1) * 512]) for i, e in enumerate(EVENTS)}
     n = min(512, (s + 127) // 128)
@@ -89,11 +90,23 @@ def main():
         "reduce: staged -> next dQ seen": med(lambda i: tr["r_dq_seen"][i + 1] - tr["r_stage_done"][i]),
         "dq freed -> dP(next) issue": med(lambda i: tr["mma_dP"][i + 1] - tr["r_dq_free"][i]),
     }
+    out.update({
+        "compute: dS done -> barrier passed": med(lambda i: tr["c_bar_passed"][i + 1] - tr["c_ds_done"][i]),
+        "compute: barrier -> s_full wait start": med(lambda i: tr["u21"][i + 1] - tr["c_bar_passed"][i + 1]),
+        "compute: s_full wait": med(lambda i: tr["c_s_seen"][i + 1] - tr["u21"][i + 1]),
+        "S(i+1) done (observer) -> compute sees": med(lambda i: tr["c_s_seen"][i + 1] - tr["done_S_next"][i]),
+        "pipe: dP done -> dV done": med(lambda i: tr["done_dV"][i] - tr["done_dP"][i]),
+        "pipe: dV done -> S(i+1) done": med(lambda i: tr["done_S_next"][i] - tr["done_dV"][i]),
+        "pipe: S(i+1) done -> dK done": med(lambda i: tr["done_dK"][i] - tr["done_S_next"][i]),
+        "pipe: dK done -> dQ done": med(lambda i: tr["done_dQ"][i] - tr["done_dK"][i]),
+        "pipe: dQ done -> dP(i+1) done": med(lambda i: tr["done_dP"][i + 1] - tr["done_dQ"][i]),
+    })
     for k, v in out.items():
         print(f"{k:36s} {v:10.0f}")
     # raw event times of three mid iterations, relative to dV issue of the first
     base = tr["mma_dV"][n // 2]
-    evs = sorted((tr[e][i] - base, e, i) for e in EVENTS[:15] for i in range(n // 2, n // 2 + 3))
+    evs = sorted((tr[e][i] - base, e, i) for e in EVENTS[:15] + EVENTS[16:21]
+                 for i in range(n // 2, n // 2 + 3))
     for t, e, i in evs:
         print(f"{t:8d}  {e:14s} it={i}")
 

@@ -42,6 +42,7 @@ def main():
     ap.add_argument("--workload", default="gpt1.3b_32k")
     ap.add_argument("--only", default="")
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--cublas", action="store_true", help="also time torch.matmul (cuBLAS) on each GEMM shape")
     args = ap.parse_args()
     h, heads, s = WL[args.workload]
     T = s
@@ -68,11 +69,17 @@ def main():
             y = torch.empty(T, nout, dtype=bf, device=dev)
             fl = 2 * T * kin * nout
             out(f"fwd_{name}", timed(lambda: K.linear(a, w, y), args.reps), fl, M=T, N=nout, K=kin)
+            if args.cublas:
+                out(f"cublas_fwd_{name}", timed(lambda: torch.matmul(a, w, out=y), args.reps), fl, M=T, N=nout, K=kin)
             dy = torch.randn(T, nout, device=dev).to(bf)
             dx = torch.empty(T, kin, dtype=bf, device=dev)
             out(f"dx_{name}", timed(lambda: K.linear_dx(dy, w, dx), args.reps), fl, M=T, N=kin, K=nout)
             acc = torch.zeros(kin, nout, device=dev)
             out(f"dw_{name}", timed(lambda: K.linear_dw(a, dy, acc), args.reps), fl, M=kin, N=nout, K=T)
+            if args.cublas:
+                wt = torch.empty(kin, nout, dtype=bf, device=dev)
+                out(f"cublas_dw_{name}", timed(lambda: torch.matmul(a.t(), dy, out=wt), args.reps), fl,
+                    M=kin, N=nout, K=T)
             del w, a, y, dy, dx, acc
         del x
         torch.cuda.empty_cache()

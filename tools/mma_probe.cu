@@ -151,6 +151,36 @@ __global__ void __launch_bounds__(128, 1) probe_contend(int iters, long long* cy
     mbar_wait(&bar, 0);
     cycles[blockIdx.x] = clock64() - t0;
     atomicExch(&stop, 1);
+  } else if (warp > 0 && ST == 4) {
+    // TMEM writes of columns 256.. by warps 1..3
+    long long n = 0;
+    const long long c0 = clock64();
+    uint32_t r[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) r[i] = i;
+    while (!*reinterpret_cast<volatile int*>(&stop)) {
+      tmem_st32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + 256 + (n & 7) * 32, r);
+      tmem_wait_st();
+      ++n;
+    }
+    if (threadIdx.x == 32 && blockIdx.x == 0) { sink[0] = static_cast<int>(n); sink[1] = static_cast<int>(clock64() - c0); }
+  } else if (warp == 1 && ST == 5) {
+    // bulk smem -> global copies (TMA engine reading smem), 16 KB each, 2 in flight
+    long long n = 0;
+    const long long c0 = clock64();
+    float* g = reinterpret_cast<float*>(sink) + 64 + blockIdx.x * 8192;
+    if (lane_id() == 0) {
+      while (!*reinterpret_cast<volatile int*>(&stop)) {
+        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 16384;" ::"l"(g),
+                     "r"(smem_u32(smem + 32768 + (n & 1) * 16384))
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        ++n;
+      }
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      if (blockIdx.x == 0) { sink[0] = static_cast<int>(n); sink[1] = static_cast<int>(clock64() - c0); }
+    }
   } else if (warp > 0 && ST == 3) {
     // TMEM reads of columns 256.. (not touched by the MMA) by warps 1..3
     long long n = 0;
@@ -202,7 +232,7 @@ void run_contend(int sms) {
   long long* d;
   int* sink;
   cudaMalloc(&d, sms * sizeof(long long));
-  cudaMalloc(&sink, 16);
+  cudaMalloc(&sink, 256 + 148 * 8192 * 4);
   cudaFuncSetAttribute(probe_contend<ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
   probe_contend<ST><<<sms, 128, 96 * 1024>>>(16, d, sink);
   probe_contend<ST><<<sms, 128, 96 * 1024>>>(iters, d, sink);
@@ -211,9 +241,10 @@ void run_contend(int sms) {
   int hs[2] = {0, 0};
   cudaMemcpy(&c0, d, sizeof(long long), cudaMemcpyDeviceToHost);
   cudaMemcpy(hs, sink, 8, cudaMemcpyDeviceToHost);
-  const double bytes_per_clk = ST == 3 ? 3.0 * 32 * 128 * hs[0] / hs[1] : ST ? 96.0 * 16 * hs[0] / hs[1] : 0.0;
+  const double bytes_per_clk = ST == 3 || ST == 4 ? 3.0 * 32 * 128 * hs[0] / hs[1]
+                             : ST == 5 ? 16384.0 * hs[0] / hs[1] : ST ? 96.0 * 16 * hs[0] / hs[1] : 0.0;
   printf("{\"form\": \"SS N=128 + %s\", \"cycles_per_mma\": %.2f, \"other_smem_B_per_clk\": %.1f}\n",
-         ST == 0 ? "idle" : ST == 1 ? "96 threads STS.128" : ST == 2 ? "96 threads LDS.128" : "3 warps tcgen05.ld x32", c0 / (8.0 * iters), bytes_per_clk);
+         ST == 0 ? "idle" : ST == 1 ? "96 threads STS.128" : ST == 2 ? "96 threads LDS.128" : ST == 3 ? "3 warps tcgen05.ld x32" : ST == 4 ? "3 warps tcgen05.st x32" : "bulk smem->global 16KB x2", c0 / (8.0 * iters), bytes_per_clk);
   cudaFree(d);
   cudaFree(sink);
 }
@@ -261,6 +292,8 @@ int main() {
   run_contend<1>(sms);
   run_contend<2>(sms);
   run_contend<3>(sms);
+  run_contend<4>(sms);
+  run_contend<5>(sms);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) printf("error %s\n", cudaGetErrorString(e));
   return 0;

@@ -1,26 +1,12 @@
-// Causal flash attention backward on tcgen05 / TMEM / TMA (sm_100a), atomic-free.
+// Causal flash attention backward on tcgen05 / TMEM / TMA (sm_100a).
 // Replaces P/runtime/mathops.py:103-116:
 //   dV = P^T dO, dP = dO V^T, dS = P (dP - D), dQ = dS K / sqrt(d), dK = dS^T Q / sqrt(d)
 // with D = rowsum(dO * O) (pre-pass) and P rebuilt from the forward's LSE.
 //
-// Two kernels, each owning one accumulator in TMEM for its whole lifetime, so
-// no cross-CTA reduction (and no atomics) is needed:
-//
-// dK/dV kernel: CTA = one 128-row key tile; streams 64-row query tiles i from
-//   the diagonal to the end.  MMA stream per tile:
-//     S^T(i+1) = K Q^T      TS (K resident in TMEM)        -> S^T[(i+1)&1]
-//     dP^T(i)  = V dO^T     SS (V resident in smem)         -> dP^T
-//     dV      += P^T dO     TS (P^T written over S^T)       [after softmax]
-//     dK      += dS^T Q     TS (dS^T written over dP^T)     [after dS]
-//   so the softmax of tile i overlaps S^T(i+1) + dP^T(i) on the tensor core.
-//   TMEM: dK 0 | dV 128 | K 256 | S^T[b] 320+64b | dP^T 448.
-// dQ kernel: CTA = one 128-row query tile; streams 64-row key tiles j = 0..diag.
-//     S(j)  = Q K^T   TS (Q resident in TMEM)   -> S[j&1], double-buffered
-//     dP(j) = dO V^T  TS (dO resident in TMEM)  -> dP[j&1]
-//     dQ   += dS K    TS (dS written over S)
-//   TMEM: S[b] 64b | dP[b] 128+64b | dQ 256 | Q 384 | dO 384+D/2.
-// Compute warps: NWG warpgroups, warpgroup g owns 64/NWG columns of each streamed
-// tile (thread = TMEM lane = resident row); 4*NWG = TMA warp, 4*NWG+1 = MMA warp.
+// Default (v10): one fused pass per 128-row key tile, dK / dV resident in TMEM,
+// dQ partials reduced into an fp32 accumulator by TMA bulk reduce-adds (see the
+// "fused (v10)" section).  HX_ATTN_BWD=9 selects the deterministic, atomic-free
+// split kernels (v9: a dK/dV kernel per key tile and a dQ kernel per query tile).
 #include "attention_common.cuh"
 
 namespace hx {
@@ -32,17 +18,6 @@ HX_DEVICE uint32_t packed_kstep(uint32_t region, int kk) {
   return region + CW * ((16 * kk) / CW) + ((16 * kk) % CW) / 2;
 }
 
-template <int CW>
-HX_DEVICE void ld_cols(uint32_t taddr, uint32_t (&r)[CW]) {
-  if constexpr (CW == 32) tmem_ld32(taddr, r);
-  else tmem_ld16(taddr, r);
-}
-template <int N>
-HX_DEVICE void st_cols(uint32_t taddr, const uint32_t (&r)[N]) {
-  if constexpr (N == 16) tmem_st16(taddr, r);
-  else tmem_st8(taddr, r);
-}
-
 // dK / dV epilogue / dQ epilogue: columns [g*D/NWG, (g+1)*D/NWG) of one row.
 template <int D, int NWG>
 HX_DEVICE void acc_row_out(uint32_t tacc, int g, __nv_bfloat16* dst, float scale, bool valid) {
@@ -51,366 +26,6 @@ HX_DEVICE void acc_row_out(uint32_t tacc, int g, __nv_bfloat16* dst, float scale
 #pragma unroll
   for (int ch = 0; ch < W / NC; ++ch)
     tmem_row_to_global<NC>(tacc + g * W + ch * NC, dst + g * W + ch * NC, scale, valid);
-}
-
-// ------------------------------------------------------------------ dK / dV
-
-template <int D>
-struct KVSmem {
-  static constexpr int STAGES = 4;
-  static constexpr int V = 0;
-  static constexpr int Q = V + Tile<D>::BYTES;             // STAGES x [64 x D]
-  static constexpr int DO = Q + STAGES * Half<D>::BYTES;   // STAGES x [64 x D]
-  static constexpr int STAT = DO + STAGES * Half<D>::BYTES;  // [2][lse2 | delta][64]
-  static constexpr int BAR = STAT + 2 * 2 * BT * 4;
-  static constexpr int TOTAL = BAR + 256;
-};
-
-template <int D, int NWG>
-__global__ void __launch_bounds__((4 * NWG + 2) * 32, 1)
-    attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_qkv128, const __grid_constant__ CUtensorMap tm_qkv64,
-                         const __grid_constant__ CUtensorMap tm_do64, const __nv_bfloat16* __restrict__ qkv,
-                         int ld_qkv, const AttnParams p) {
-  using L = KVSmem<D>;
-  constexpr int ST = L::STAGES;
-  constexpr int CW = BT / NWG;           // query columns per warpgroup
-  constexpr int NT = 128 * NWG;          // compute threads
-  constexpr int TMA_WARP = 4 * NWG, MMA_WARP = 4 * NWG + 1;
-  extern __shared__ __align__(1024) uint8_t smem[];
-  if ((smem_u32(smem) & 1023) != 0) __trap();
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR);
-  uint64_t* qdo_full = bars;              // ST
-  uint64_t* qdo_empty = bars + ST;        // ST
-  uint64_t* v_full = bars + 2 * ST;
-  uint64_t* k_ready = bars + 2 * ST + 1;  // NT arrivals
-  uint64_t* s_full = bars + 2 * ST + 2;   // 2
-  uint64_t* dp_full = bars + 2 * ST + 4;
-  uint64_t* p_full = bars + 2 * ST + 5;   // NT arrivals
-  uint64_t* ds_full = bars + 2 * ST + 6;  // NT arrivals
-  uint64_t* acc_full = bars + 2 * ST + 7;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * ST + 8);
-  constexpr int NBARS = 2 * ST + 8;
-  float* stat = reinterpret_cast<float*>(smem + L::STAT);
-
-  const int warp = warp_id(), lane = lane_id();
-  const int nq = (p.s + BT - 1) / BT;
-  const int kt = static_cast<int>(blockIdx.x);  // heaviest key tiles first
-  const int bh = blockIdx.y;
-  const int bi = bh / p.heads, head = bh % p.heads;
-  const int qcol = head * D, vcol = 2 * p.h + head * D;
-  const int q_first = 2 * kt;  // first 64-row query tile that sees this key tile
-  const int n_it = nq - q_first;
-
-  if (warp == TMA_WARP && lane == 0) {
-    tma_prefetch(&tm_qkv128);
-    tma_prefetch(&tm_qkv64);
-    tma_prefetch(&tm_do64);
-    for (int i = 0; i < NBARS; ++i) {
-      const bool many = i == 2 * ST + 1 || i == 2 * ST + 5 || i == 2 * ST + 6;
-      mbar_init(&bars[i], many ? NT : 1);
-    }
-    fence_barrier_init();
-  }
-  if (warp == MMA_WARP) tmem_alloc(tmem_slot, 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t tDK = tmem, tDV = tmem + 128, tK = tmem + 256, tS0 = tmem + 320, tDP = tmem + 448;
-
-  if (warp == TMA_WARP) {
-    if (lane == 0) {
-      mbar_arrive_expect_tx(v_full, Tile<D>::BYTES);
-      tma_tile_rows<D>(smem + L::V, &tm_qkv128, v_full, vcol, bi, kt * AT_TILE, AT_TILE);
-      for (int it = 0; it < n_it; ++it) {
-        const int st = it % ST, q0 = (q_first + it) * BT;
-        mbar_wait(&qdo_empty[st], ((it / ST) & 1) ^ 1);
-        mbar_arrive_expect_tx(&qdo_full[st], 2 * Half<D>::BYTES);
-        tma_tile_rows<D>(smem + L::Q + st * Half<D>::BYTES, &tm_qkv64, &qdo_full[st], qcol, bi, q0, BT);
-        tma_tile_rows<D>(smem + L::DO + st * Half<D>::BYTES, &tm_do64, &qdo_full[st], head * D, bi, q0, BT);
-      }
-    }
-  } else if (warp == MMA_WARP) {
-    if (lane == 0) {
-      constexpr uint32_t id_sp = idesc_bf16(128, BT, false, false);
-      constexpr uint32_t id_kv = idesc_bf16(128, D, false, true);
-      const uint32_t sv = smem_u32(smem + L::V);
-      auto sq = [&](int it) { return smem_u32(smem + L::Q + (it % ST) * Half<D>::BYTES); };
-      auto sdo = [&](int it) { return smem_u32(smem + L::DO + (it % ST) * Half<D>::BYTES); };
-      auto issue_s = [&](int it) {
-        mbar_wait(&qdo_full[it % ST], (it / ST) & 1);
-        tc_fence_after();
-        const uint32_t ts = tS0 + 64 * (it & 1);
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) umma_f16_ts(ts, tK + kk * 8, kdesc(sq(it), kk, BT), id_sp, kk > 0);
-        umma_commit(&s_full[it & 1]);
-      };
-      mbar_wait(k_ready, 0);
-      mbar_wait(v_full, 0);
-      tc_fence_after();
-      issue_s(0);
-      for (int it = 0; it < n_it; ++it) {
-        // dP^T(i) first: it is the one smem-fed (slower) MMA and the softmax of
-        // tile i needs it right after P(i); S^T(i+1) follows.
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          umma_f16_ss(tDP, kdesc(sv, kk, AT_TILE), kdesc(sdo(it), kk, BT), id_sp, kk > 0);
-        umma_commit(dp_full);
-        if (it + 1 < n_it) issue_s(it + 1);
-        mbar_wait(p_full, it & 1);
-        tc_fence_after();
-        const uint32_t ts = tS0 + 64 * (it & 1);
-#pragma unroll
-        for (int kk = 0; kk < BT / 16; ++kk)
-          umma_f16_ts(tDV, packed_kstep<CW>(ts, kk), mndesc(sdo(it), kk, BT), id_kv, it > 0 || kk > 0);
-        mbar_wait(ds_full, it & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < BT / 16; ++kk)
-          umma_f16_ts(tDK, packed_kstep<CW>(tDP, kk), mndesc(sq(it), kk, BT), id_kv, it > 0 || kk > 0);
-        umma_commit(&qdo_empty[it % ST]);
-      }
-      umma_commit(acc_full);
-    }
-  } else {
-    // ---------------- compute: thread = key row c, query columns [qoff, qoff + CW)
-    const int g = warp >> 2, quad = warp & 3;
-    const int c = quad * 32 + lane;
-    const int qoff = CW * g;
-    const int ct = threadIdx.x;
-    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
-    const int64_t row_base = static_cast<int64_t>(bh) * p.s;
-    const int kv_row = kt * AT_TILE + c;
-    const int64_t kv_tok = static_cast<int64_t>(kv_row) * p.b + bi;
-    row_to_tmem<D / NWG>(tK + lane_off + g * (D / NWG / 2), qkv + kv_tok * ld_qkv + p.h + head * D + g * (D / NWG),
-                         kv_row < p.s);
-    tmem_wait_st();
-    tc_fence_before();
-    mbar_arrive(k_ready);
-    // lse2 / delta of the next query tile are fetched one tile ahead
-    float nxt = 0.f;
-    auto fetch = [&](int it) {
-      const int qi = ct & (BT - 1), q = (q_first + it) * BT + qi;
-      if (ct < BT) nxt = q < p.s ? p.lse[row_base + q] * LOG2E : 0.f;
-      else if (ct < 2 * BT) nxt = q < p.s ? p.delta[row_base + q] : 0.f;
-    };
-    fetch(0);
-    for (int it = 0; it < n_it; ++it) {
-      const int q0 = (q_first + it) * BT;
-      float* s_lse = stat + (it & 1) * 2 * BT;
-      float* s_del = s_lse + BT;
-      if (ct < 2 * BT) (ct < BT ? s_lse : s_del)[ct & (BT - 1)] = nxt;
-      named_barrier_sync(1, NT);
-      if (it + 1 < n_it) fetch(it + 1);
-      const bool need_mask = q0 < (kt + 1) * AT_TILE || q0 + BT > p.s;
-      const uint32_t ts = tS0 + 64 * (it & 1);
-      float lv[CW];
-#pragma unroll
-      for (int v = 0; v < CW / 4; ++v) {
-        const float4 t4 = reinterpret_cast<const float4*>(s_lse + qoff)[v];
-        lv[4 * v] = t4.x; lv[4 * v + 1] = t4.y; lv[4 * v + 2] = t4.z; lv[4 * v + 3] = t4.w;
-      }
-      mbar_wait(&s_full[it & 1], (it >> 1) & 1);
-      tc_fence_after();
-      uint32_t raw[CW];
-      ld_cols<CW>(ts + lane_off + qoff, raw);
-      tmem_wait_ld();
-      float pv[CW];
-      uint32_t pk[CW / 2];
-#pragma unroll
-      for (int j = 0; j < CW; ++j) pv[j] = fast_exp2(fmaf(__uint_as_float(raw[j]), p.scale_log2, -lv[j]));
-      if (need_mask) {  // the two query tiles overlapping this key tile, and the sequence tail
-#pragma unroll
-        for (int j = 0; j < CW; ++j)
-          if (q0 + qoff + j < kv_row || q0 + qoff + j >= p.s) pv[j] = 0.f;
-      }
-#pragma unroll
-      for (int j = 0; j < CW / 2; ++j) pk[j] = pack_bf16(pv[2 * j], pv[2 * j + 1]);
-      st_cols<CW / 2>(ts + lane_off + qoff, pk);  // P^T over this warpgroup's own S^T columns
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(p_full);
-#pragma unroll
-      for (int v = 0; v < CW / 4; ++v) {
-        const float4 t4 = reinterpret_cast<const float4*>(s_del + qoff)[v];
-        lv[4 * v] = t4.x; lv[4 * v + 1] = t4.y; lv[4 * v + 2] = t4.z; lv[4 * v + 3] = t4.w;
-      }
-      mbar_wait(dp_full, it & 1);
-      tc_fence_after();
-      ld_cols<CW>(tDP + lane_off + qoff, raw);
-      tmem_wait_ld();
-#pragma unroll
-      for (int j = 0; j < CW / 2; ++j)
-        pk[j] = pack_bf16(pv[2 * j] * (__uint_as_float(raw[2 * j]) - lv[2 * j]),
-                          pv[2 * j + 1] * (__uint_as_float(raw[2 * j + 1]) - lv[2 * j + 1]));
-      st_cols<CW / 2>(tDP + lane_off + qoff, pk);  // dS^T over this warpgroup's own dP^T columns
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(ds_full);
-    }
-    mbar_wait(acc_full, 0);
-    tc_fence_after();
-    __nv_bfloat16* dst = p.dqkv + kv_tok * p.ld_dqkv + head * D;
-    acc_row_out<D, NWG>(tDK + lane_off, g, dst + p.h, p.scale, kv_row < p.s);
-    acc_row_out<D, NWG>(tDV + lane_off, g, dst + 2 * p.h, 1.f, kv_row < p.s);
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == MMA_WARP) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 512);
-  }
-}
-
-// ------------------------------------------------------------------ dQ
-
-template <int D>
-struct QSmem {
-  static constexpr int STAGES = 4;
-  static constexpr int KV = 0;  // STAGES x (K, V) [64 x D]
-  static constexpr int BAR = KV + STAGES * 2 * Half<D>::BYTES;
-  static constexpr int TOTAL = BAR + 256;
-};
-
-template <int D, int NWG>
-__global__ void __launch_bounds__((4 * NWG + 2) * 32, 1)
-    attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_qkv64, const __nv_bfloat16* __restrict__ qkv,
-                       int ld_qkv, const __nv_bfloat16* __restrict__ d_o, int ld_o, const AttnParams p) {
-  using L = QSmem<D>;
-  constexpr int ST = L::STAGES;
-  constexpr int CW = BT / NWG;  // key columns per warpgroup
-  constexpr int NT = 128 * NWG;
-  constexpr int TMA_WARP = 4 * NWG, MMA_WARP = 4 * NWG + 1;
-  extern __shared__ __align__(1024) uint8_t smem[];
-  if ((smem_u32(smem) & 1023) != 0) __trap();
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR);
-  uint64_t* kv_full = bars;                 // ST
-  uint64_t* kv_empty = bars + ST;           // ST
-  uint64_t* sdp_full = bars + 2 * ST;       // 2
-  uint64_t* ds_full = bars + 2 * ST + 2;    // NT arrivals
-  uint64_t* qdo_ready = bars + 2 * ST + 3;  // NT arrivals
-  uint64_t* dq_done = bars + 2 * ST + 4;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * ST + 5);
-  constexpr int NBARS = 2 * ST + 5;
-
-  const int warp = warp_id(), lane = lane_id();
-  const int nq = (p.s + AT_TILE - 1) / AT_TILE;
-  const int qt = nq - 1 - static_cast<int>(blockIdx.x);  // heaviest query tiles first
-  const int q_last = min(p.s, (qt + 1) * AT_TILE) - 1;
-  const int nkv = q_last / BT + 1;
-  const int bh = blockIdx.y;
-  const int bi = bh / p.heads, head = bh % p.heads;
-  const int kcol = p.h + head * D, vcol = 2 * p.h + head * D;
-
-  if (warp == TMA_WARP && lane == 0) {
-    tma_prefetch(&tm_qkv64);
-    for (int i = 0; i < NBARS; ++i) mbar_init(&bars[i], (i == 2 * ST + 2 || i == 2 * ST + 3) ? NT : 1);
-    fence_barrier_init();
-  }
-  if (warp == MMA_WARP) tmem_alloc(tmem_slot, 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t tS0 = tmem, tDP0 = tmem + 128, tDQ = tmem + 256, tQ = tmem + 384, tDO = tmem + 384 + D / 2;
-
-  if (warp == TMA_WARP) {
-    if (lane == 0) {
-      for (int j = 0; j < nkv; ++j) {
-        const int st = j % ST;
-        mbar_wait(&kv_empty[st], ((j / ST) & 1) ^ 1);
-        uint8_t* kb = smem + L::KV + st * 2 * Half<D>::BYTES;
-        mbar_arrive_expect_tx(&kv_full[st], 2 * Half<D>::BYTES);
-        tma_tile_rows<D>(kb, &tm_qkv64, &kv_full[st], kcol, bi, j * BT, BT);
-        tma_tile_rows<D>(kb + Half<D>::BYTES, &tm_qkv64, &kv_full[st], vcol, bi, j * BT, BT);
-      }
-    }
-  } else if (warp == MMA_WARP) {
-    if (lane == 0) {
-      constexpr uint32_t id_sp = idesc_bf16(128, BT, false, false);
-      constexpr uint32_t id_q = idesc_bf16(128, D, false, true);
-      auto skv = [&](int j) { return smem_u32(smem + L::KV + (j % ST) * 2 * Half<D>::BYTES); };
-      auto issue_sdp = [&](int j) {
-        const int b = j & 1;
-        mbar_wait(&kv_full[j % ST], (j / ST) & 1);
-        tc_fence_after();
-        const uint32_t sk = skv(j), sv = sk + Half<D>::BYTES;
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          umma_f16_ts(tS0 + 64 * b, tQ + kk * 8, kdesc(sk, kk, BT), id_sp, kk > 0);
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          umma_f16_ts(tDP0 + 64 * b, tDO + kk * 8, kdesc(sv, kk, BT), id_sp, kk > 0);
-        umma_commit(&sdp_full[b]);
-      };
-      mbar_wait(qdo_ready, 0);
-      tc_fence_after();
-      issue_sdp(0);
-      for (int j = 0; j < nkv; ++j) {
-        if (j + 1 < nkv) issue_sdp(j + 1);
-        mbar_wait(ds_full, j & 1);
-        tc_fence_after();
-        const uint32_t tds = tS0 + 64 * (j & 1);
-#pragma unroll
-        for (int kk = 0; kk < BT / 16; ++kk)
-          umma_f16_ts(tDQ, packed_kstep<CW>(tds, kk), mndesc(skv(j), kk, BT), id_q, j > 0 || kk > 0);
-        umma_commit(&kv_empty[j % ST]);
-      }
-      umma_commit(dq_done);
-    }
-  } else {
-    // ---------------- compute: thread = query row r, key columns [koff, koff + CW)
-    const int g = warp >> 2, quad = warp & 3;
-    const int r = quad * 32 + lane;
-    const int koff = CW * g;
-    const int q = qt * AT_TILE + r;
-    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
-    const int64_t tok = static_cast<int64_t>(q) * p.b + bi;
-    row_to_tmem<D / NWG>(tQ + lane_off + g * (D / NWG / 2), qkv + tok * ld_qkv + head * D + g * (D / NWG), q < p.s);
-    row_to_tmem<D / NWG>(tDO + lane_off + g * (D / NWG / 2), d_o + tok * ld_o + head * D + g * (D / NWG), q < p.s);
-    tmem_wait_st();
-    tc_fence_before();
-    mbar_arrive(qdo_ready);
-    const int64_t row = static_cast<int64_t>(bh) * p.s + q;
-    const float lse2 = q < p.s ? p.lse[row] * LOG2E : 0.f;
-    const float dlt = q < p.s ? p.delta[row] : 0.f;
-    for (int j = 0; j < nkv; ++j) {
-      const int b = j & 1;
-      mbar_wait(&sdp_full[b], (j >> 1) & 1);
-      tc_fence_after();
-      uint32_t rs[CW], rd[CW];
-      ld_cols<CW>(tS0 + 64 * b + lane_off + koff, rs);
-      ld_cols<CW>(tDP0 + 64 * b + lane_off + koff, rd);
-      tmem_wait_ld();
-      const int k0 = j * BT + koff;
-      float pv[CW];
-#pragma unroll
-      for (int i = 0; i < CW; ++i) pv[i] = fast_exp2(fmaf(__uint_as_float(rs[i]), p.scale_log2, -lse2));
-      if (k0 + CW - 1 > qt * AT_TILE) {  // tile crosses the diagonal
-#pragma unroll
-        for (int i = 0; i < CW; ++i)
-          if (k0 + i > q) pv[i] = 0.f;
-      }
-      uint32_t pk[CW / 2];
-#pragma unroll
-      for (int i = 0; i < CW / 2; ++i)
-        pk[i] = pack_bf16(pv[2 * i] * (__uint_as_float(rd[2 * i]) - dlt),
-                          pv[2 * i + 1] * (__uint_as_float(rd[2 * i + 1]) - dlt));
-      st_cols<CW / 2>(tS0 + 64 * b + lane_off + koff, pk);  // dS over this warpgroup's own S columns
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(ds_full);
-    }
-    mbar_wait(dq_done, 0);
-    tc_fence_after();
-    acc_row_out<D, NWG>(tDQ + lane_off, g, p.dqkv + tok * p.ld_dqkv + head * D, p.scale, q < p.s);
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == MMA_WARP) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 512);
-  }
 }
 
 // =====================================================================================
@@ -1256,39 +871,6 @@ __global__ void __launch_bounds__(256) attn_bwd_pre_kernel(const __nv_bfloat16* 
 
 // ------------------------------------------------------------------ host side
 
-template <int D, int NWG>
-static cudaError_t bwd_launch(const void* qkv, int ld_qkv, const void* o, const void* d_o, int ld_o,
-                              const AttnParams& p, cudaStream_t st) {
-  CUtensorMap tq128, tq64, tdo64;
-  cudaError_t e = make_tma_3d_rows(&tq128, qkv, 3 * p.h, p.b, p.s, ld_qkv, 64, AT_TILE);
-  if (e == cudaSuccess) e = make_tma_3d_rows(&tq64, qkv, 3 * p.h, p.b, p.s, ld_qkv, 64, BT);
-  if (e == cudaSuccess) e = make_tma_3d_rows(&tdo64, d_o, p.h, p.b, p.s, ld_o, 64, BT);
-  if (e != cudaSuccess) return e;
-  static bool cfg = false;
-  if (!cfg) {
-    e = cudaFuncSetAttribute(attn_bwd_dkdv_kernel<D, NWG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             KVSmem<D>::TOTAL);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(attn_bwd_dq_kernel<D, NWG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               QSmem<D>::TOTAL);
-    if (e != cudaSuccess) return e;
-    cfg = true;
-  }
-  const int tokens = p.s * p.b;
-  attn_bwd_pre_kernel<D><<<(tokens + 7) / 8, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(o),
-                                                           static_cast<const __nv_bfloat16*>(d_o), ld_o,
-                                                           const_cast<float*>(p.delta), p.s, p.b, p.heads);
-  dim3 grid((p.s + AT_TILE - 1) / AT_TILE, p.b * p.heads);
-  constexpr int threads = (4 * NWG + 2) * 32;
-  attn_bwd_dkdv_kernel<D, NWG><<<grid, threads, KVSmem<D>::TOTAL, st>>>(
-      tq128, tq64, tdo64, static_cast<const __nv_bfloat16*>(qkv), ld_qkv, p);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  attn_bwd_dq_kernel<D, NWG><<<grid, threads, QSmem<D>::TOTAL, st>>>(
-      tq64, static_cast<const __nv_bfloat16*>(qkv), ld_qkv, static_cast<const __nv_bfloat16*>(d_o), ld_o, p);
-  return cudaGetLastError();
-}
-
 template <int D>
 static cudaError_t bwd9_launch(const void* qkv, int ld_qkv, const void* o, const void* d_o, int ld_o,
                                const AttnParams& p, cudaStream_t st) {
@@ -1372,23 +954,15 @@ cudaError_t attn_bwd_launch(const void* qkv, int ld_qkv, const void* o, const vo
   p.dqkv = static_cast<__nv_bfloat16*>(dqkv);
   p.ld_dqkv = ld_dqkv;
   // Default: the fused one-pass kernel (v10).  HX_ATTN_BWD=9 selects the split
-  // atomic-free dK/dV + dQ kernels, 8 the 64-wide split kernels, for A/B runs.
+  // atomic-free dK/dV + dQ kernels (deterministic dq; also for A/B runs).
   static const int variant = getenv("HX_ATTN_BWD") ? atoi(getenv("HX_ATTN_BWD")) : 10;
   if (variant == 10) {
     if (d == 128) return fused_launch<128>(qkv, ld_qkv, o, d_o, ld_o, dq_acc, p, st);
     if (d == 64) return fused_launch<64>(qkv, ld_qkv, o, d_o, ld_o, dq_acc, p, st);
     return cudaErrorNotSupported;
   }
-  if (variant == 9) {
-    if (d == 128) return bwd9_launch<128>(qkv, ld_qkv, o, d_o, ld_o, p, st);
-    if (d == 64) return bwd9_launch<64>(qkv, ld_qkv, o, d_o, ld_o, p, st);
-    return cudaErrorNotSupported;
-  }
-  static const int nwg = getenv("HX_ATTN_NWG") ? atoi(getenv("HX_ATTN_NWG")) : 2;
-  if (d == 128) return nwg == 2 ? bwd_launch<128, 2>(qkv, ld_qkv, o, d_o, ld_o, p, st)
-                                : bwd_launch<128, 4>(qkv, ld_qkv, o, d_o, ld_o, p, st);
-  if (d == 64) return nwg == 2 ? bwd_launch<64, 2>(qkv, ld_qkv, o, d_o, ld_o, p, st)
-                               : bwd_launch<64, 4>(qkv, ld_qkv, o, d_o, ld_o, p, st);
+  if (d == 128) return bwd9_launch<128>(qkv, ld_qkv, o, d_o, ld_o, p, st);
+  if (d == 64) return bwd9_launch<64>(qkv, ld_qkv, o, d_o, ld_o, p, st);
   return cudaErrorNotSupported;
 }
 

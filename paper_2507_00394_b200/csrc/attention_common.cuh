@@ -14,17 +14,12 @@
 namespace hx {
 
 constexpr int AT_TILE = 128;  // rows of a resident (M-side) tile
-constexpr int BT = 64;        // rows of a streamed tile in the backward kernels
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
 
 template <int D>
 struct Tile {  // [128 x D]
   static constexpr int BYTES = AT_TILE * D * 2;
-};
-template <int D>
-struct Half {  // [64 x D]
-  static constexpr int BYTES = BT * D * 2;
 };
 
 struct AttnParams {

@@ -11,6 +11,32 @@ namespace hx {
 
 constexpr float LN_EPS = 1e-5f;
 
+// One warp per row, two passes over the row: pass 1 reads it from HBM and
+// accumulates the row sums (sum and sum of squares in one sweep), pass 2
+// re-reads it (an L1/L2 hit) to write the output.  Nothing row-sized stays live
+// across the warp reductions, so registers stay low and enough warps per SM
+// keep HBM busy.  var = E[x^2] - mu^2 in fp32 over bf16 inputs: the
+// cancellation error is ~1e-7 * mu^2/var relative, far below bf16 output rounding.
+HX_DEVICE void unpack8(const uint4& u, float (&f)[8]) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 t = unpack_bf16(w[j]);
+    f[2 * j] = t.x;
+    f[2 * j + 1] = t.y;
+  }
+}
+HX_DEVICE void load_gain8(const float* __restrict__ g, int c, float (&f)[8]) {
+  const float4 a = reinterpret_cast<const float4*>(g)[2 * c];
+  const float4 b = reinterpret_cast<const float4*>(g)[2 * c + 1];
+  f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+}
+HX_DEVICE float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 template <int NV>  // NV = 16-byte vectors (8 bf16) per lane
 __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16* __restrict__ x,
                                                       const float* __restrict__ gain,
@@ -22,61 +48,45 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16* __rest
   const int lane = lane_id();
   const int nvec = h / 8;
   const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<int64_t>(row) * h);
-  float v[NV][8];
-  float sum = 0.f;
+  float sum = 0.f, sq = 0.f;
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
     const int c = lane + 32 * i;
     if (c < nvec) {
-      uint4 u = xr[c];
-      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+      float f[8];
+      unpack8(xr[c], f);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float2 f = unpack_bf16(w[j]);
-        v[i][2 * j] = f.x;
-        v[i][2 * j + 1] = f.y;
-        sum += f.x + f.y;
+      for (int j = 0; j < 8; ++j) {
+        sum += f[j];
+        sq = fmaf(f[j], f[j], sq);
       }
     }
   }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  sum = warp_sum(sum);
+  sq = warp_sum(sq);
   const float mu = sum / h;
-  float sq = 0.f;
-#pragma unroll
-  for (int i = 0; i < NV; ++i)
-    if (lane + 32 * i < nvec)
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float d = v[i][j] - mu;
-        sq += d * d;
-      }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-  const float rstd = rsqrtf(sq / h + LN_EPS);
+  const float rstd = rsqrtf(fmaxf(sq / h - mu * mu, 0.f) + LN_EPS);
   uint4* yr = reinterpret_cast<uint4*>(y + static_cast<int64_t>(row) * h);
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
     const int c = lane + 32 * i;
     if (c < nvec) {
-      const float4 g0 = reinterpret_cast<const float4*>(gain)[2 * c];
-      const float4 g1 = reinterpret_cast<const float4*>(gain)[2 * c + 1];
-      const float4 b0 = reinterpret_cast<const float4*>(bias)[2 * c];
-      const float4 b1 = reinterpret_cast<const float4*>(bias)[2 * c + 1];
-      const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-      const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-      float o[8];
+      float f[8], g[8], bb[8], o[8];
+      unpack8(xr[c], f);
+      load_gain8(gain, c, g);
+      load_gain8(bias, c, bb);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) o[j] = (v[i][j] - mu) * rstd * g[j] + bb[j];
+      for (int j = 0; j < 8; ++j) o[j] = (f[j] - mu) * rstd * g[j] + bb[j];
       yr[c] = make_uint4(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]), pack_bf16(o[4], o[5]),
                          pack_bf16(o[6], o[7]));
     }
   }
 }
 
-// LN backward, input-gradient half: one warp per row, row data in registers,
-// dx = rstd*(dy*g - mean(dy*g) - xhat*mean(dy*g*xhat)) (+ dres).  Also stores
-// the row's (mean, rstd) for the column-reduction kernel below.
+// LN backward, input-gradient half: one warp per row,
+// dx = rstd*(dy*g - mean(dy*g) - xhat*mean(dy*g*xhat)) (+ dres).  Pass 1 gathers
+// sum x, sum x^2, sum dy*g, sum dy*g*x in one sweep; pass 2 re-reads x, dy and
+// writes dx.  Also stores the row's (mean, rstd) for the column reduction below.
 template <int NV>
 __global__ void __launch_bounds__(256) ln_bwd_dx_kernel(
     const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
@@ -87,75 +97,50 @@ __global__ void __launch_bounds__(256) ln_bwd_dx_kernel(
   const int lane = lane_id();
   const int nvec = h / 8;
   const int64_t off = static_cast<int64_t>(row) * h;
-  float xv[NV][8], gv[NV][8];
-  float sx = 0.f, sxx = 0.f;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + off);
+  const uint4* dr = reinterpret_cast<const uint4*>(dy + off);
+  float sx = 0.f, sxx = 0.f, sg = 0.f, sgx = 0.f;
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
     const int c = lane + 32 * i;
     if (c < nvec) {
-      const uint4 ux = reinterpret_cast<const uint4*>(x + off)[c];
-      const uint4 ud = reinterpret_cast<const uint4*>(dy + off)[c];
-      const float4 g0 = reinterpret_cast<const float4*>(gain)[2 * c];
-      const float4 g1 = reinterpret_cast<const float4*>(gain)[2 * c + 1];
-      const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-      const uint32_t wx[4] = {ux.x, ux.y, ux.z, ux.w}, wd[4] = {ud.x, ud.y, ud.z, ud.w};
+      float f[8], d[8], g[8];
+      unpack8(xr[c], f);
+      unpack8(dr[c], d);
+      load_gain8(gain, c, g);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float2 fx = unpack_bf16(wx[j]), fd = unpack_bf16(wd[j]);
-        xv[i][2 * j] = fx.x;
-        xv[i][2 * j + 1] = fx.y;
-        gv[i][2 * j] = fd.x * gg[2 * j];  // dxhat = dy * gain
-        gv[i][2 * j + 1] = fd.y * gg[2 * j + 1];
-        sx += fx.x + fx.y;
+      for (int j = 0; j < 8; ++j) {
+        const float gd = d[j] * g[j];  // dxhat = dy * gain
+        sx += f[j];
+        sxx = fmaf(f[j], f[j], sxx);
+        sg += gd;
+        sgx = fmaf(gd, f[j], sgx);
       }
     }
   }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) sx += __shfl_xor_sync(0xffffffffu, sx, o);
+  sx = warp_sum(sx);
+  sxx = warp_sum(sxx);
+  sg = warp_sum(sg);
+  sgx = warp_sum(sgx);
   const float mu = sx / h;
-#pragma unroll
-  for (int i = 0; i < NV; ++i)
-    if (lane + 32 * i < nvec)
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float d = xv[i][j] - mu;
-        sxx += d * d;
-      }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) sxx += __shfl_xor_sync(0xffffffffu, sxx, o);
-  const float rstd = rsqrtf(sxx / h + LN_EPS);
-  float s1 = 0.f, s2 = 0.f;
-#pragma unroll
-  for (int i = 0; i < NV; ++i)
-    if (lane + 32 * i < nvec)
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        xv[i][j] = (xv[i][j] - mu) * rstd;
-        s1 += gv[i][j];
-        s2 += gv[i][j] * xv[i][j];
-      }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-  }
-  const float m1 = s1 / h, m2 = s2 / h;
+  const float rstd = rsqrtf(fmaxf(sxx / h - mu * mu, 0.f) + LN_EPS);
+  const float m1 = sg / h;                          // mean(dxhat)
+  const float m2 = (sgx / h - mu * m1) * rstd;      // mean(dxhat * xhat)
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
     const int c = lane + 32 * i;
     if (c < nvec) {
-      float o[8];
+      float f[8], d[8], g[8], o[8];
+      unpack8(xr[c], f);
+      unpack8(dr[c], d);
+      load_gain8(gain, c, g);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) o[j] = rstd * (gv[i][j] - m1 - xv[i][j] * m2);
+      for (int j = 0; j < 8; ++j) o[j] = rstd * (d[j] * g[j] - m1 - (f[j] - mu) * rstd * m2);
       if (dres) {
-        const uint4 ur = reinterpret_cast<const uint4*>(dres + off)[c];
-        const uint32_t wr[4] = {ur.x, ur.y, ur.z, ur.w};
+        float r[8];
+        unpack8(reinterpret_cast<const uint4*>(dres + off)[c], r);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float2 f = unpack_bf16(wr[j]);
-          o[2 * j] += f.x;
-          o[2 * j + 1] += f.y;
-        }
+        for (int j = 0; j < 8; ++j) o[j] += r[j];
       }
       reinterpret_cast<uint4*>(dx + off)[c] =
           make_uint4(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]), pack_bf16(o[4], o[5]), pack_bf16(o[6], o[7]));

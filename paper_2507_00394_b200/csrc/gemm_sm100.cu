@@ -9,6 +9,10 @@
 //   b_mn = 0 : B stored [N, K] (K contiguous)   -> UMMA K-major  (input grads, dY * W^T)
 //   b_mn = 1 : B stored [K, N] (N contiguous)   -> UMMA MN-major (forward, X * W)
 //
+// Default for large GEMMs: gemm_2sm_kernel, CTA pairs (cta_group::2) computing
+// 256 x 256 tiles with 256x256x16 MMAs (see its comment).  The single-CTA kernel
+// below serves GEMMs too small to pair.
+//
 // Structure (one CTA per SM, 256 threads):
 //   warp 0 lane 0 : TMA producer, STAGES-deep smem ring (128B-swizzled tiles)
 //   warp 1 lane 0 : UMMA issuer, 128 x BN x 16 tcgen05.mma, accumulator in TMEM,
@@ -277,6 +281,190 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
 }
 
+
+// ------------------------------------------------------------------ 2-CTA (cta_group::2)
+// One 256 x 256 output tile per CTA pair: the leader issues 256x256x16 MMAs whose
+// A rows and B columns come half from each CTA's smem, so each SM stages only
+// its own 128 A rows and 128 B columns per k-block (32 KB instead of 48 KB):
+// 6 stages in flight instead of 4, and half the L2->SM traffic for B.
+// Both CTAs' TMA loads complete on the leader's full barrier; the leader's
+// commits release both CTAs' stages (empty) and accumulators (tfull); both
+// CTAs' epilogue threads return accumulators on the leader's tempty barrier.
+constexpr int G2_STAGES = 6;
+constexpr int G2_A_BYTES = GEMM_BM * GEMM_BK * 2;   // 16 KB: this CTA's 128 rows
+constexpr int G2_B_BYTES = 128 * GEMM_BK * 2;       // 16 KB: this CTA's 128 of 256 columns
+constexpr int G2_STAGE_BYTES = G2_A_BYTES + G2_B_BYTES;
+constexpr int G2_BAR_OFFSET = G2_STAGES * G2_STAGE_BYTES;
+constexpr int G2_SMEM_BYTES = G2_BAR_OFFSET + 256 + 1024;
+
+template <bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    gemm_2sm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+                    const GemmParams p) {
+  constexpr int BN = 256;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + G2_BAR_OFFSET);
+  uint64_t* empty = full + G2_STAGES;
+  uint64_t* tfull = empty + G2_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const int rank = static_cast<int>(cluster_ctarank());
+  const bool leader = rank == 0;
+  const int num_m = (p.M + GEMM_BM - 1) / GEMM_BM;
+  const int num_n = (p.N + BN - 1) / BN;
+  const int num_k = (p.K + GEMM_BK - 1) / GEMM_BK;
+  const int num_tiles = (num_m / 2) * num_n;
+  const int first = static_cast<int>(cluster_id_x());
+  const int stride = static_cast<int>(nclusters_x());
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm_a);
+    tma_prefetch(&tm_b);
+    for (int s = 0; s < G2_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 256);  // epilogue threads of both CTAs
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_2sm(tmem_slot, 2 * BN);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer (both CTAs): own A rows + own half of B
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = first; t < num_tiles; t += stride) {
+        int mp, nb;
+        tile_coords(t, num_m / 2, num_n, mp, nb);
+        const int m0 = (2 * mp + rank) * GEMM_BM, n0 = nb * BN + rank * 128;
+        for (int kb = 0; kb < num_k; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          const uint32_t bar = mapa_shared(&full[stage], 0);
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * G2_STAGE_BYTES);
+          uint8_t* sa = smem + stage * G2_STAGE_BYTES;
+          uint8_t* sb = sa + G2_A_BYTES;
+          const int k0 = kb * GEMM_BK;
+          if (A_MN) {
+            tma_load_2d_2sm(sa, &tm_a, bar, m0, k0);
+            tma_load_2d_2sm(sa + 8192, &tm_a, bar, m0 + 64, k0);
+          } else {
+            tma_load_2d_2sm(sa, &tm_a, bar, k0, m0);
+          }
+          if (B_MN) {
+            tma_load_2d_2sm(sb, &tm_b, bar, n0, k0);
+            tma_load_2d_2sm(sb + 8192, &tm_b, bar, n0 + 64, k0);
+          } else {
+            tma_load_2d_2sm(sb, &tm_b, bar, k0, n0);
+          }
+          if (++stage == G2_STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      // ---------------- UMMA issuer (pair leader): 256 x 256 x 16 per instruction
+      constexpr uint32_t idesc = idesc_bf16(2 * GEMM_BM, BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = first; t < num_tiles; t += stride, ++it) {
+        const int acc = it & 1;
+        mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_k; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * G2_STAGE_BYTES);
+          const uint32_t sb = sa + G2_A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < GEMM_BK / 16; ++kk) {
+            const uint64_t da = A_MN ? sw128_desc(sa + kk * 2048, 8192, 1024)
+                                     : sw128_desc(sa + kk * 32, 16, 1024);
+            const uint64_t db = B_MN ? sw128_desc(sb + kk * 2048, 8192, 1024)
+                                     : sw128_desc(sb + kk * 32, 16, 1024);
+            umma_f16_ss_2sm(d_tmem, da, db, idesc, (kb | kk) != 0);
+          }
+          umma_commit_2sm_mc(&empty[stage], 0x3);
+          if (++stage == G2_STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit_2sm_mc(&tfull[acc], 0x3);
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue (both CTAs): this CTA's 128 rows of the 256 x 256 tile
+    const int sub = warp & 3;
+    const uint32_t tempty_leader0 = mapa_shared(&tempty[0], 0);
+    int it = 0;
+    for (int t = first; t < num_tiles; t += stride, ++it) {
+      int mp, nb;
+      tile_coords(t, num_m / 2, num_n, mp, nb);
+      const int acc = it & 1;
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const int row = (2 * mp + rank) * GEMM_BM + sub * 32 + lane;
+      const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(sub * 32) << 16);
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        const int col = nb * BN + c * 32;
+        if (col >= p.N) break;  // warp-uniform
+        uint32_t r[32];
+        tmem_ld32(taddr + c * 32, r);
+        tmem_wait_ld();
+        epilogue_chunk(p, row, col, r);
+      }
+      tc_fence_before();
+      mbar_arrive_cluster(tempty_leader0 + acc * 8);
+    }
+  }
+  __syncthreads();
+  cluster_sync();  // the peer's smem / barriers stay valid until both CTAs are done
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_2sm(tmem_base, 2 * BN);
+  }
+}
+
+template <bool A_MN, bool B_MN>
+static cudaError_t launch_gemm_2sm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
+                                   int num_sms, cudaStream_t stream) {
+  auto kern = gemm_2sm_kernel<A_MN, B_MN>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G2_SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const int pairs = ((p.M + GEMM_BM - 1) / GEMM_BM / 2) * ((p.N + 255) / 256);
+  int grid = 2 * (pairs < num_sms / 2 ? pairs : num_sms / 2);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.dynamicSmemBytes = G2_SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, ta, tb, p);
+}
+
 // ------------------------------------------------------------------ host side
 
 template <int BN, bool A_MN, bool B_MN, bool CL>
@@ -340,10 +528,22 @@ cudaError_t gemm_launch(const GemmOperand& a, const GemmOperand& b, const GemmPa
   if (e != cudaSuccess) return e;
   // 2-CTA clusters with B multicast when the M-blocks pair up evenly and there are
   // enough tile pairs to fill the machine (HX_GEMM_CLUSTER=0 disables, for A/B runs)
-  static const bool allow_cl = !getenv("HX_GEMM_CLUSTER") || atoi(getenv("HX_GEMM_CLUSTER")) != 0;
+  // HX_GEMM_CLUSTER: 2 (default) cta_group::2 pairs, 1 B-multicast pairs, 0 single CTAs
+  static const int cl_mode = getenv("HX_GEMM_CLUSTER") ? atoi(getenv("HX_GEMM_CLUSTER")) : 2;
   const int num_m = (p.M + GEMM_BM - 1) / GEMM_BM;
-  const bool cl = allow_cl && bn == 256 && num_m % 2 == 0 &&
-                  (num_m / 2) * ((p.N + bn - 1) / bn) >= num_sms / 2;
+  const int pairs = (num_m / 2) * ((p.N + 255) / 256);
+  const bool pairable = bn == 256 && num_m % 2 == 0 && pairs >= num_sms / 2;
+  const bool cl = cl_mode != 0 && pairable;
+  // cta_group::2 also wins with fewer tiles than pairs of SMs (e.g. the 2048 x 2048
+  // weight gradient: 64 pairs); only tiny GEMMs stay on single CTAs
+  if (cl_mode == 2 && num_m % 2 == 0 && p.N > 128 && pairs >= 32) {
+    e = b.mn ? make_tma_2d(&tb, b.ptr, p.K, p.N, b.ld, 64, 64) : make_tma_2d(&tb, b.ptr, p.N, p.K, b.ld, 64, 128);
+    if (e != cudaSuccess) return e;
+    if (a.mn && b.mn) return launch_gemm_2sm<true, true>(ta, tb, p, num_sms, stream);
+    if (!a.mn && b.mn) return launch_gemm_2sm<false, true>(ta, tb, p, num_sms, stream);
+    if (!a.mn && !b.mn) return launch_gemm_2sm<false, false>(ta, tb, p, num_sms, stream);
+    return cudaErrorNotSupported;
+  }
   e = b.mn ? make_tma_2d(&tb, b.ptr, p.K, p.N, b.ld, 64, 64)
            : make_tma_2d(&tb, b.ptr, p.N, p.K, b.ld, 64, cl ? bn / 2 : bn);
   if (e != cudaSuccess) return e;

@@ -59,6 +59,9 @@ def parse():
                     help="device budget for stashed activations; the rest is FILO-offloaded to pinned "
                          "host memory ('auto': free HBM after weights/grads minus a working-set margin; "
                          "default: auto for gpt7b_128k, off otherwise)")
+    ap.add_argument("--trace-out", default=None,
+                    help="write the measured per-task device timeline of one iteration as a Chrome "
+                         "trace (<prefix>.trace.json) and CSV (<prefix>.csv), reference schema")
     ap.add_argument("--compare-1f1b", choices=["auto", "yes", "no"], default="auto",
                     help="also time the same-kernel 1F1B schedule (default: only when N > 1)")
     return ap.parse_args()
@@ -330,6 +333,10 @@ def main() -> None:
         dist.all_gather_object(allt, tl)
         tl = {k: v for part in allt for k, v in part.items()}
     predicted = None
+    if rank == 0 and tl and args.trace_out:
+        from paper_2507_00394_b200.simulate import timeline_csv, write_chrome_trace
+        write_chrome_trace(f"{args.trace_out}.trace.json", sched, tl, "ms")
+        Path(f"{args.trace_out}.csv").write_text(timeline_csv(sched, tl))
     if rank == 0 and tl:
         measured = metrics_from_timeline(sched, tl)
         bubble = measured.bubble_fraction

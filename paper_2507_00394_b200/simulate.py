@@ -133,3 +133,46 @@ def simulate(sched: Schedule, durations: DurationTable, comm: CommModel | None =
     res = replay(sched, make_duration_fn(durations, fused), comm or CommModel.zero())
     return SimResult(sched, res.timeline,
                      metrics_from_timeline(sched, res.timeline, durations.time_unit))
+
+
+# --- exports (reference schema, ``P/simulate.py:157-196``) -------------------------------
+
+
+def chrome_trace(sched: Schedule, timeline, time_unit: str = "ms") -> list[dict]:
+    """Chrome trace-event list of a (simulated or device-measured) timeline:
+    pid = stage, tid = lane ("compute", "in" for RECV, "out" for SEND), ts / dur
+    in microseconds, args = (kind, comp, mb, layer), the reference's schema.
+    ``time_unit``: "ms" (CUDA-event timelines), "ns", or "units" (1:1)."""
+    from .schedule import RECV
+    scale = {"ms": 1e3, "ns": 1e-3}.get(time_unit, 1.0)
+    events = []
+    for tid in sorted(timeline):
+        t = sched.tasks[tid]
+        start, end = timeline[tid]
+        lane = {SEND: "out", RECV: "in"}.get(t.kind, "compute")
+        events.append({
+            "name": tid, "ph": "X", "pid": t.stage, "tid": lane,
+            "ts": start * scale, "dur": (end - start) * scale, "cat": t.kind,
+            "args": {"kind": t.kind, "comp": t.comp, "mb": t.mb, "layer": t.layer},
+        })
+    return events
+
+
+def write_chrome_trace(path, sched: Schedule, timeline, time_unit: str = "ms") -> None:
+    import json
+    from pathlib import Path
+    Path(path).write_text(json.dumps({"traceEvents": chrome_trace(sched, timeline, time_unit)}, indent=1))
+
+
+def timeline_csv(sched: Schedule, timeline) -> str:
+    """Task intervals as CSV (task, stage, kind, mb, layer, start, end), sorted by
+    (start, end, task) like the reference's export."""
+    import csv
+    import io
+    buf = io.StringIO()
+    w = csv.writer(buf, lineterminator="\n")
+    w.writerow(["task", "stage", "kind", "mb", "layer", "start", "end"])
+    for tid, (start, end) in sorted(timeline.items(), key=lambda kv: (kv[1][0], kv[1][1], kv[0])):
+        t = sched.tasks[tid]
+        w.writerow([tid, t.stage, t.kind, t.mb, t.layer, start, end])
+    return buf.getvalue()

@@ -450,10 +450,10 @@ struct FusedSmem {
   static constexpr int TOTAL = BAR + 256;
 };
 
-template <int D, bool RED>
+template <int D>
 __global__ void __launch_bounds__(512, 1)
     attn_bwd_fused_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
-                          const __grid_constant__ CUtensorMap tm_dq, float* __restrict__ dq_acc, const AttnParams p) {
+                          const __grid_constant__ CUtensorMap tm_dq, const AttnParams p) {
   using L = FusedSmem<D>;
   constexpr int NT = 256;  // compute threads
   constexpr bool DQ_SHARES_DP = 2 * D + 256 + D > 512;
@@ -636,70 +636,38 @@ __global__ void __launch_bounds__(512, 1)
     regs_inc<136>();
     const int quad = warp & 3, r = quad * 32 + lane, rt = threadIdx.x - 384;
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
-    if constexpr (RED) {
-      // register path: red.global.add.v2 straight from the 16x256b TMEM fragments
-      // (4 threads cover one full 32-byte sector; no smem traffic at all)
-      for (int it = 0; it < n_it; ++it) {
-        mbar_wait(dq_full, it & 1);
-        tc_fence_after();
-        if (rt == 0) HX_BT(9, it);
-        uint32_t v[2][64];
-        tmem_ld_16x256b_x16(tDQ + lane_off, v[0]);
-        tmem_ld_16x256b_x16(tDQ + lane_off + (16u << 16), v[1]);  // (D = 64: columns >= 64 unused)
-        tmem_wait_ld();
-        tc_fence_before();
-        mbar_arrive(dq_empty);
-        if (rt == 0) HX_BT(10, it);
-        const int q0 = (kt + it) * AT_TILE;
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {  // TMEM lanes quad*32 + 16*hh ..
-#pragma unroll
-          for (int rr = 0; rr < 2; ++rr) {
-            const int row = quad * 32 + 16 * hh + (lane >> 2) + 8 * rr;
-            if (q0 + row < p.s) {
-              float* dst = dq_acc + (static_cast<int64_t>(bh) * p.s + q0 + row) * D + 2 * (lane & 3);
-#pragma unroll
-              for (int c = 0; c < 16; ++c)
-                if (8 * c < D) red_add_v2(dst + 8 * c, v[hh][4 * c + 2 * rr], v[hh][4 * c + 2 * rr + 1]);
-            }
-          }
-        }
-        if (rt == 0) HX_BT(11, it);
-      }
-    } else {
     uint8_t* stg = smem + L::STG;
-      int k = 0;
-      for (int it = 0; it < n_it; ++it) {
-        mbar_wait(dq_full, it & 1);
-        tc_fence_after();
-        if (rt == 0) HX_BT(9, it);
-        uint32_t v[D];
-  #pragma unroll
-        for (int c = 0; c < D / 32; ++c) tmem_ld32(tDQ + lane_off + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
-        tmem_wait_ld();
-        tc_fence_before();
-        mbar_arrive(dq_empty);
-        if (rt == 0) HX_BT(10, it);
-        const int q0 = (kt + it) * AT_TILE;
-        if (kNoReduce) continue;
-  #pragma unroll
-        for (int c = 0; c < D / 32; ++c, ++k) {
-          uint8_t* buf = stg + (k & 1) * (AT_TILE * 128);
-          if (rt == 0) bulk_wait_read<1>();
-          named_barrier_sync(2, 128);
-  #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            *reinterpret_cast<uint4*>(buf + r * 128 + ((j ^ (r & 7)) << 4)) =
-                make_uint4(v[32 * c + 4 * j], v[32 * c + 4 * j + 1], v[32 * c + 4 * j + 2], v[32 * c + 4 * j + 3]);
-          fence_proxy_async();
-          named_barrier_sync(2, 128);
-          if (rt == 0) {
-            tma_reduce_add_3d(&tm_dq, buf, 32 * c, q0, bh);
-            bulk_commit();
-          }
+    int k = 0;
+    for (int it = 0; it < n_it; ++it) {
+      mbar_wait(dq_full, it & 1);
+      tc_fence_after();
+      if (rt == 0) HX_BT(9, it);
+      uint32_t v[D];
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) tmem_ld32(tDQ + lane_off + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(dq_empty);
+      if (rt == 0) HX_BT(10, it);
+      const int q0 = (kt + it) * AT_TILE;
+      if (kNoReduce) continue;
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c, ++k) {
+        uint8_t* buf = stg + (k & 1) * (AT_TILE * 128);
+        if (rt == 0) bulk_wait_read<1>();
+        named_barrier_sync(2, 128);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<uint4*>(buf + r * 128 + ((j ^ (r & 7)) << 4)) =
+              make_uint4(v[32 * c + 4 * j], v[32 * c + 4 * j + 1], v[32 * c + 4 * j + 2], v[32 * c + 4 * j + 3]);
+        fence_proxy_async();
+        named_barrier_sync(2, 128);
+        if (rt == 0) {
+          tma_reduce_add_3d(&tm_dq, buf, 32 * c, q0, bh);
+          bulk_commit();
         }
-        if (rt == 0) HX_BT(11, it);
       }
+      if (rt == 0) HX_BT(11, it);
     }
     if (rt == 0) bulk_wait_all();
     finish();
@@ -908,16 +876,10 @@ static cudaError_t fused_launch(const void* qkv, int ld_qkv, const void* o, cons
   if (e == cudaSuccess) e = make_tma_3d_rows(&tdo, d_o, p.h, p.b, p.s, ld_o, 64, AT_TILE);
   if (e == cudaSuccess) e = make_tma_f32_3d(&tdq, dq_acc, D, p.s, static_cast<uint64_t>(p.b) * p.heads, 32, AT_TILE);
   if (e != cudaSuccess) return e;
-  // dQ reduction path: TMA bulk reduce-add through smem staging (default) or
-  // red.global from registers (HX_DQ_RED=1), for A/B runs.
-  static const bool red = getenv("HX_DQ_RED") && atoi(getenv("HX_DQ_RED")) != 0;
   static bool cfg = false;
   if (!cfg) {
-    e = cudaFuncSetAttribute(attn_bwd_fused_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(attn_bwd_fused_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              FusedSmem<D>::TOTAL);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(attn_bwd_fused_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               FusedSmem<D>::TOTAL);
     if (e != cudaSuccess) return e;
     cfg = true;
   }
@@ -928,10 +890,7 @@ static cudaError_t fused_launch(const void* qkv, int ld_qkv, const void* o, cons
                                                            static_cast<const __nv_bfloat16*>(d_o), ld_o,
                                                            const_cast<float*>(p.delta), p.s, p.b, p.heads);
   dim3 grid((p.s + AT_TILE - 1) / AT_TILE, p.b * p.heads);
-  if (red)
-    attn_bwd_fused_kernel<D, true><<<grid, 512, FusedSmem<D>::TOTAL, st>>>(tq, tdo, tdq, dq_acc, p);
-  else
-    attn_bwd_fused_kernel<D, false><<<grid, 512, FusedSmem<D>::TOTAL, st>>>(tq, tdo, tdq, dq_acc, p);
+  attn_bwd_fused_kernel<D><<<grid, 512, FusedSmem<D>::TOTAL, st>>>(tq, tdo, tdq, p);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int64_t vecs = static_cast<int64_t>(tokens) * p.h / 8;

@@ -63,7 +63,8 @@ def parse():
                     help="write the measured per-task device timeline of one iteration as a Chrome "
                          "trace (<prefix>.trace.json) and CSV (<prefix>.csv), reference schema")
     ap.add_argument("--compare-1f1b", choices=["auto", "yes", "no"], default="auto",
-                    help="also time the same-kernel 1F1B schedule (default: only when N > 1)")
+                    help="also time the same-kernel 1F1B schedule on the same model / inputs "
+                         "(auto: yes, except for the host-offload workload gpt7b_128k)")
     return ap.parse_args()
 
 
@@ -353,7 +354,7 @@ def main() -> None:
 
     # same-kernel 1F1B baseline (the north-star comparison), same model / inputs
     base_1f1b = None
-    if args.compare_1f1b == "yes" or (args.compare_1f1b == "auto" and world > 1):
+    if args.compare_1f1b == "yes" or (args.compare_1f1b == "auto" and args.workload != "gpt7b_128k"):
         del rt
         torch.cuda.empty_cache()
         rt_b = build_runtime(generate("1f1b", cfg, units))

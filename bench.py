@@ -357,11 +357,12 @@ def main() -> None:
     if args.compare_1f1b == "yes" or (args.compare_1f1b == "auto" and args.workload != "gpt7b_128k"):
         del rt
         torch.cuda.empty_cache()
-        rt_b = build_runtime(generate("1f1b", cfg, units))
+        base_method = "1f1b_rc" if args.method.endswith("_rc") else "1f1b"  # like for like
+        rt_b = build_runtime(generate(base_method, cfg, units))
         for _ in range(max(1, args.warmup)):
             rt_b.run(inputs)
         ms_b = time_steps(rt_b, args.steps)
-        base_1f1b = {"value": tokens / (ms_b / 1e3), "ms_per_step": ms_b,
+        base_1f1b = {"method": base_method, "value": tokens / (ms_b / 1e3), "ms_per_step": ms_b,
                      "helix_speedup": ms_b / ms}
         del rt_b
         torch.cuda.empty_cache()

@@ -68,14 +68,18 @@ class CommModel:
 _PASS_OF = {FWD: "fwd", RECOMPUTE: "fwd", BWD_B: "bwd_b", BWD_W: "bwd_w"}
 
 
-def make_duration_fn(table, fused_backward: bool = False):
-    """Task -> integer duration; a fused BWD_B also bills the weight pass."""
+def make_duration_fn(table, fused_backward: bool = False, chunk_recompute: bool = False):
+    """Task -> integer duration; a fused BWD_B also bills the weight pass.
+    ``chunk_recompute`` (B200 extension, ``1f1b_rc``): a chunk's backward also
+    re-runs the pre and post forward of each of its layers."""
 
     def duration(task: Task) -> int:
         pass_ = _PASS_OF[task.kind]
         if task.comp == "chunk":
             total = task.span * table.comp_totals(pass_)
             extra = task.span * table.comp_totals("bwd_w")
+            if chunk_recompute and task.kind == BWD_B:
+                total += task.span * (table.of("pre", "fwd") + table.of("post", "fwd"))
         else:
             total = table.of(task.comp, pass_)
             extra = table.of(task.comp, "bwd_w")

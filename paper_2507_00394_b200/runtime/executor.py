@@ -296,9 +296,15 @@ class _Core:
         deferred = []
         for l in range(t.layer + t.span - 1, t.layer - 1, -1):
             W, G = self.W(l), self.G(l)
-            gap, w_post = self.math.post_backward_b(d, W, G, st.stash.pop((l, t.mb, "post")))
-            gpa = self.math.attn_backward(gap, st.stash.pop((l, t.mb, "attn")))
-            d, w_pre = self.math.pre_backward_b(gpa, W, G, st.stash.pop((l, t.mb, "pre")))
+            s_post = st.stash.pop((l, t.mb, "post"))
+            s_attn = st.stash.pop((l, t.mb, "attn"))
+            s_pre = st.stash.pop((l, t.mb, "pre"))
+            if self.rc:  # 1f1b_rc: regenerate this layer's non-attention stash in place
+                s_post = self.math.regenerate_stash("post", s_post, W)
+                s_pre = self.math.regenerate_stash("pre", s_pre, W)
+            gap, w_post = self.math.post_backward_b(d, W, G, s_post)
+            gpa = self.math.attn_backward(gap, s_attn)
+            d, w_pre = self.math.pre_backward_b(gpa, W, G, s_pre)
             if self.split:
                 deferred.append((l, w_post, w_pre))
             else:

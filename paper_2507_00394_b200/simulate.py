@@ -97,7 +97,8 @@ def measured_durations(sched: Schedule, timeline) -> DurationTable:
 
 
 def predict_pipeline(cfg, durations: DurationTable, stages=(2, 4, 8), link_gbs: float = 770.0,
-                     latency_us: float = 5.0, methods=("helix_twofold", "helix_twofold_rc", "1f1b")) -> dict:
+                     latency_us: float = 5.0,
+                     methods=("helix_twofold", "helix_twofold_rc", "1f1b", "1f1b_rc")) -> dict:
     """Predicted throughput of each method at p stages (m = 2p, weak scaling),
     from measured per-component durations (ns) and an NVLink transfer model
     (bytes over ``link_gbs`` per direction + latency) in the reference's own
@@ -124,13 +125,19 @@ def predict_pipeline(cfg, durations: DurationTable, stages=(2, 4, 8), link_gbs: 
             for method in methods:
                 if method != "1f1b":
                     row[method]["speedup_vs_1f1b"] = (row["1f1b"]["makespan_ms"] / row[method]["makespan_ms"])
+        if "1f1b_rc" in row and "helix_twofold_rc" in row:
+            # like for like when the full stash does not fit: both with recomputation
+            row["helix_twofold_rc"]["speedup_vs_1f1b_rc"] = (row["1f1b_rc"]["makespan_ms"] /
+                                                            row["helix_twofold_rc"]["makespan_ms"])
         out[f"p{p}"] = row
     return out
 
 
 def simulate(sched: Schedule, durations: DurationTable, comm: CommModel | None = None) -> SimResult:
     fused = sched.meta.get("backward") == "fused"
-    res = replay(sched, make_duration_fn(durations, fused), comm or CommModel.zero())
+    chunk_rc = bool(int(sched.meta.get("recompute", 0))) and any(
+        t.comp == "chunk" for t in sched.tasks.values() if t.is_compute)
+    res = replay(sched, make_duration_fn(durations, fused, chunk_rc), comm or CommModel.zero())
     return SimResult(sched, res.timeline,
                      metrics_from_timeline(sched, res.timeline, durations.time_unit))
 

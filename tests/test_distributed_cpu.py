@@ -16,7 +16,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from oracle import helix_oracle as O
-from paper_2507_00394_b200 import METHODS, ModelConfig, generate
+from paper_2507_00394_b200 import EXTENSION_METHODS, METHODS, ModelConfig, generate
 from paper_2507_00394_b200.costs import DurationTable
 from paper_2507_00394_b200.runtime.executor import (
     DeviceModel, HelixRuntime, P2PPlan, _gather_distributed, make_pair_groups, stage_fields)
@@ -83,7 +83,7 @@ TOY2 = dict(L=4, h=8, s=8, b=2, num_heads=2, p=2, m=4)
 TOY4 = dict(L=4, h=8, s=8, b=1, num_heads=2, p=4, m=8)
 
 
-@pytest.mark.parametrize("method", METHODS)
+@pytest.mark.parametrize("method", METHODS + EXTENSION_METHODS)
 def test_two_ranks_every_method_matches_oracle(method):
     losses, grads, peaks = run_world(2, TOY2, method)
     ref = _oracle(TOY2)

@@ -2,8 +2,8 @@
 s=32768), where the float64 oracle cannot run (it materialises [b, n, s, s]).
 
 * schedule invariance: every method (helix naive / two-fold / two-fold + rc,
-  1F1B, ZB1P) computes the same losses and gradients from the same weights and
-  inputs, within the bf16 tolerances of test_parity_gpu.py;
+  1F1B, ZB1P, and the 1F1B + recompute extension) computes the same losses
+  and gradients from the same weights and inputs;
 * an independent fp32 PyTorch model of the reference block (LayerNorm, QKV,
   causal softmax attention via SDPA, output projection, LayerNorm, erf-GeLU MLP,
   mean(z^2) loss; P/runtime/layers.py:94-137, model.py:61-64) on the same bf16
@@ -104,7 +104,7 @@ def test_schedule_invariance_at_full_size(weights_inputs):
     layers, inputs = weights_inputs
     base_l, base_g = run_method("helix_twofold", layers, inputs)
     assert all(np.isfinite(base_l))
-    for method in ("helix_naive", "helix_twofold_rc", "1f1b", "zb1p"):
+    for method in ("helix_naive", "helix_twofold_rc", "1f1b", "zb1p", "1f1b_rc"):
         l, g = run_method(method, layers, inputs)
         compare(l, g, base_l, base_g, f"{method} vs helix_twofold")
 

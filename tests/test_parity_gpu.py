@@ -73,7 +73,7 @@ def test_every_method_matches_oracle_small(method):
     compare(res, oracle_for(SMALL), SMALL.L, f"small {method}")
 
 
-@pytest.mark.parametrize("method", ["helix_twofold", "helix_twofold_rc", "1f1b"])
+@pytest.mark.parametrize("method", ["helix_twofold", "helix_twofold_rc", "1f1b", "1f1b_rc"])
 def test_head_dim_128_batch_2_matches_oracle(method):
     compare(run(WIDE, method), oracle_for(WIDE), WIDE.L, f"wide {method}")
 

@@ -101,3 +101,29 @@ def test_simulated_1f1b_bubble_fraction():
         res = simulate(generate("1f1b", cfg, DurationTable.from_units(1, 3, 2)),
                        DurationTable.from_units(1, 3, 2))
         assert res.metrics.bubble_fraction == pytest.approx((p - 1) / (m + p - 1))
+
+
+def test_1f1b_rc_extension_schedule():
+    """B200 extension: 1F1B with recomputation-without-attention inside chunks.
+    Same tasks and order as 1F1B, stash accounting at the recompute retention,
+    and the chunk backward billed with the re-run pre / post forward."""
+    from paper_2507_00394_b200 import ModelConfig, generate, validate_schedule
+    from paper_2507_00394_b200.costs import DurationTable, layer_activation_elements
+    from paper_2507_00394_b200.simulate import simulate
+
+    cfg = ModelConfig(L=4, h=64, s=128, b=1, num_heads=2, p=2, m=4)
+    units = DurationTable.from_units(1, 3, 2)
+    base, rc = generate("1f1b", cfg, units), generate("1f1b_rc", cfg, units)
+    validate_schedule(rc)
+    assert rc.method == "1f1b_rc" and int(rc.meta["recompute"]) == 1
+    assert sorted(base.tasks) == sorted(rc.tasks) and base.per_stage_order == rc.per_stage_order
+    span = cfg.L // cfg.p
+    f = rc.tasks["f.s0.m0"]
+    assert f.mem_delta == layer_activation_elements(cfg, recompute=True) * span
+    assert rc.tasks["b.s0.m0"].mem_delta == -f.mem_delta
+    # the rc chunk backward costs span * (pre fwd + post fwd) more
+    sb, sr = simulate(base, units), simulate(rc, units)
+    db = sb.timeline["b.s0.m0"][1] - sb.timeline["b.s0.m0"][0]
+    dr = sr.timeline["b.s0.m0"][1] - sr.timeline["b.s0.m0"][0]
+    assert dr - db == span * (units.of("pre", "fwd") + units.of("post", "fwd"))
+    assert sr.metrics.makespan > sb.metrics.makespan

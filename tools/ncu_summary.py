@@ -38,7 +38,7 @@ UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1, "us"
 
 
 def short(name: str) -> str:
-    m = re.search(r"(attn_\w+|gemm_sm100_kernel|ln_\w+_kernel|mse_loss_kernel|axpy_f32_kernel)", name)
+    m = re.search(r"(attn_\w+|gemm_sm100_kernel|gemm_2sm_kernel|ln_\w+_kernel|mse_loss_kernel|axpy_f32_kernel)", name)
     base = m.group(1) if m else name[:40]
     t = re.search(r"<([^>]*)>", name)
     return f"{base}<{t.group(1)}>" if t else base

@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="gpt1.3b_32k", choices=sorted(WORKLOADS))
     ap.add_argument("--method", default="helix_twofold")
+    ap.add_argument("--seq", type=int, default=None, help="override the workload's sequence length (sweeps)")
     ap.add_argument("--mlp-chunk", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -217,7 +218,9 @@ def profile_traffic(kernel: str) -> float | None:
 
 def main() -> None:
     args = parse()
-    wl = WORKLOADS[args.workload]
+    wl = dict(WORKLOADS[args.workload])
+    if args.seq:
+        wl["s"] = args.seq
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))

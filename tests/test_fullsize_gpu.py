@@ -114,3 +114,37 @@ def test_full_size_against_torch_fp32(weights_inputs):
     ref_l, ref_g = torch_reference(layers, inputs)
     l, g = run_method("helix_twofold", layers, inputs)
     compare(l, g, ref_l, ref_g, "helix_twofold vs torch fp32")
+
+
+def test_stage_count_invariance_at_full_size():
+    """The same model run as a 1-, 2- and 4-stage helix pipeline (all stages on
+    this GPU, replay driver): the partition changes, the math does not."""
+    cfg1 = ModelConfig(L=4, h=2048, s=32768, b=1, num_heads=16, p=1, m=8)
+    gen = torch.Generator(device=DEV).manual_seed(11)
+    layers = [random_device_layer(cfg1.h, gen, DEV) for _ in range(cfg1.L)]
+    ig = torch.Generator(device=DEV).manual_seed(12)
+    inputs = [torch.randn(cfg1.s, cfg1.h, generator=ig, device=DEV).to(torch.bfloat16) for _ in range(cfg1.m)]
+    results = {}
+    for p in (1, 2, 4):
+        cfg = cfg1.with_(p=p)
+        sched = generate("helix_twofold", cfg, UNIT)
+        model = DeviceModel({l: DeviceLayer(dict(w), PARAM_FIELDS) for l, w in enumerate(layers)})
+        rt = HelixRuntime(sched, model, None, "replay", DEV)
+        rt.run(inputs)
+        torch.cuda.synchronize()
+        results[p] = (rt.losses(), {l: {k: g.clone() for k, g in dl.grad.items()} for l, dl in model.layers.items()})
+        del rt, model
+        torch.cuda.empty_cache()
+    base_l, base_g = results[1]
+    for p in (2, 4):
+        l, g = results[p]
+        worst_cos, worst_max = 1.0, 0.0
+        for a, b in zip(l, base_l):
+            assert abs(a - b) / abs(b) <= LOSS_TOL
+        for li in range(cfg1.L):
+            for k in PARAM_FIELDS:
+                x, y = g[li][k].double().flatten(), base_g[li][k].double().flatten()
+                worst_cos = min(worst_cos, float(x @ y / (x.norm() * y.norm())))
+                worst_max = max(worst_max, float((x - y).abs().max() / y.abs().max()))
+        print(f"[full-size] helix_twofold p={p} vs p=1: cos {worst_cos:.6f} max {worst_max:.2e}")
+        assert worst_cos >= COS_TOL and worst_max <= MAX_TOL

@@ -708,7 +708,7 @@ __global__ void __launch_bounds__(512, 1)
       tc_fence_after();
       if (ct == 0) HX_BT(5, it);
       if (ct == 224) HX_BT(14, it);
-      uint32_t raw[64];
+      uint32_t raw[32];
       if (kNoCompute) {
         tc_fence_before();
         mbar_arrive(p_full);
@@ -717,28 +717,32 @@ __global__ void __launch_bounds__(512, 1)
         mbar_arrive(ds_full);
         continue;
       }
-      tmem_ld32(tS + lane_off + qoff, *reinterpret_cast<uint32_t(*)[32]>(raw));
-      tmem_ld32(tS + lane_off + qoff + 32, *reinterpret_cast<uint32_t(*)[32]>(raw + 32));
-      tmem_wait_ld();
+      // Both phases run in 32-column halves (TMEM -> registers -> TMEM), so only
+      // P (64 fp32) stays live across the phases: no register spills at 136.
       float pv[64];
 #pragma unroll
-      for (int v = 0; v < 32; ++v) {
-        const float2 l2 = reinterpret_cast<const float2*>(s_nl + qoff)[v];
-        const float2 x = f2unpack(ffma2(f2pack(__uint_as_float(raw[2 * v]), __uint_as_float(raw[2 * v + 1])),
-                                        scale2, f2pack(l2.x, l2.y)));
-        pv[2 * v] = fast_exp2(x.x);
-        pv[2 * v + 1] = fast_exp2(x.y);
-      }
-      if (need_mask) {  // diagonal tile (query < key) and the sequence tail
+      for (int hh = 0; hh < 2; ++hh) {
+        tmem_ld32(tS + lane_off + qoff + 32 * hh, *reinterpret_cast<uint32_t(*)[32]>(raw));
+        tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 64; ++j)
-          if (q0 + qoff + j < kv_row || q0 + qoff + j >= p.s) pv[j] = 0.f;
-      }
-      {
-        uint32_t pk[32];
+        for (int v = 0; v < 16; ++v) {
+          const float2 l2 = reinterpret_cast<const float2*>(s_nl + qoff + 32 * hh)[v];
+          const float2 x = f2unpack(ffma2(f2pack(__uint_as_float(raw[2 * v]), __uint_as_float(raw[2 * v + 1])),
+                                          scale2, f2pack(l2.x, l2.y)));
+          pv[32 * hh + 2 * v] = fast_exp2(x.x);
+          pv[32 * hh + 2 * v + 1] = fast_exp2(x.y);
+        }
+        if (need_mask) {  // diagonal tile (query < key) and the sequence tail
 #pragma unroll
-        for (int j = 0; j < 32; ++j) pk[j] = pack_bf16(pv[2 * j], pv[2 * j + 1]);
-        tmem_st32(tS + lane_off + qoff, pk);  // P^T over this warpgroup's S^T columns
+          for (int j = 0; j < 32; ++j) {
+            const int q = q0 + qoff + 32 * hh + j;
+            if (q < kv_row || q >= p.s) pv[32 * hh + j] = 0.f;
+          }
+        }
+        uint32_t pk[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(pv[32 * hh + 2 * j], pv[32 * hh + 2 * j + 1]);
+        tmem_st16(tS + lane_off + qoff + 16 * hh, pk);  // P^T over S^T columns already read
       }
       tmem_wait_st();
       tc_fence_before();
@@ -747,23 +751,23 @@ __global__ void __launch_bounds__(512, 1)
       mbar_wait(dp_full, it & 1);
       tc_fence_after();
       if (ct == 0) HX_BT(7, it);
-      tmem_ld32(tDP + lane_off + qoff, *reinterpret_cast<uint32_t(*)[32]>(raw));
-      tmem_ld32(tDP + lane_off + qoff + 32, *reinterpret_cast<uint32_t(*)[32]>(raw + 32));
-      tmem_wait_ld();
-      {
-        uint32_t pk[32];
 #pragma unroll
-        for (int v = 0; v < 32; ++v) {
-          const float2 d2 = reinterpret_cast<const float2*>(s_nd + qoff)[v];
+      for (int hh = 0; hh < 2; ++hh) {
+        tmem_ld32(tDP + lane_off + qoff + 32 * hh, *reinterpret_cast<uint32_t(*)[32]>(raw));
+        tmem_wait_ld();
+        uint32_t pk[16];
+#pragma unroll
+        for (int v = 0; v < 16; ++v) {
+          const float2 d2 = reinterpret_cast<const float2*>(s_nd + qoff + 32 * hh)[v];
           const float2 ds = f2unpack(fmul2(fadd2(f2pack(__uint_as_float(raw[2 * v]), __uint_as_float(raw[2 * v + 1])),
                                                  f2pack(d2.x, d2.y)),
-                                           f2pack(pv[2 * v], pv[2 * v + 1])));
+                                           f2pack(pv[32 * hh + 2 * v], pv[32 * hh + 2 * v + 1])));
           pk[v] = pack_bf16(ds.x, ds.y);
         }
-        tmem_st32(tDP + lane_off + qoff, pk);  // dS^T over this warpgroup's dP^T columns
+        tmem_st16(tDP + lane_off + qoff + 16 * hh, pk);  // dS^T over dP^T columns already read
 #pragma unroll
-        for (int j = 0; j < 8; ++j)  // dS^T row c, query columns 64g + 8j.. (SW128 atom g)
-          *reinterpret_cast<uint4*>(sds_row + ((j ^ (c & 7)) << 4)) =
+        for (int j = 0; j < 4; ++j)  // dS^T row c, query columns 64g + 32hh + 8j.. (SW128 atom g)
+          *reinterpret_cast<uint4*>(sds_row + (((4 * hh + j) ^ (c & 7)) << 4)) =
               make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
       }
       fence_proxy_async();

@@ -117,9 +117,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         const uint32_t sv = smem_u32(slot_addr(2 * jt + 1));
         const uint32_t tP = tmem + 128 * g, tO = tmem + 256 + 128 * g;
         HX_TR(2, 2 * jt + g);
+        const uint64_t dv = sw128_desc(sv, AT_TILE * 128, 1024);  // MN-major V, +2048 B per K-step
 #pragma unroll
         for (int kk = 0; kk < AT_TILE / 16; ++kk)
-          umma_f16_ts(tO, tP + kk * 8, mndesc(sv, kk, AT_TILE), id_o, (jt > 0 || kk > 0));
+          umma_f16_ts(tO, tP + kk * 8, dv + 128 * kk, id_o, (jt > 0 || kk > 0));
         pending[g] = false;
       };
       for (int j = 0; j < nkv; ++j) {
@@ -134,9 +135,13 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
             wait_slot(2 * j);
             const uint32_t sk = smem_u32(slot_addr(2 * j));
             const uint32_t tS = tmem + 128 * g;
+            // descriptors as one base + compile-time offsets (64-col atoms, +32 B per step)
+            const uint64_t dq = sw128_desc(sq[g], 16, 1024), dk = sw128_desc(sk, 16, 1024);
 #pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk)
-              umma_f16_ss(tS, kdesc(sq[g], kk, AT_TILE), kdesc(sk, kk, AT_TILE), id_s, kk > 0);
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const uint32_t off = ((kk >> 2) * AT_TILE * 128 + (kk & 3) * 32) >> 4;
+              umma_f16_ss(tS, dq + off, dk + off, id_s, kk > 0);
+            }
             umma_commit(&s_full[g]);
             HX_TR(3, 2 * j + g);
             pending[g] = true;

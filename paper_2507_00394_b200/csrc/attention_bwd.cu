@@ -432,7 +432,7 @@ constexpr bool kNoReduce = false;
 // with the most query tiles), read back with hx_debug_bwd_trace (tools/bwd_trace.py).
 __device__ long long g_bwd_trace[16][512];
 #define HX_BT(slot, idx) \
-  if (blockIdx.x == 0 && blockIdx.y == 0 && (idx) < 512) g_bwd_trace[slot][idx] = clock64()
+  if (blockIdx.x == 0 && (idx) < 512) g_bwd_trace[slot][idx] = clock64()
 #else
 #define HX_BT(slot, idx)
 #endif
@@ -480,8 +480,11 @@ __global__ void __launch_bounds__(512, 1)
 
   const int warp = warp_id(), lane = lane_id();
   const int nq = (p.s + AT_TILE - 1) / AT_TILE;
-  const int kt = static_cast<int>(blockIdx.x);  // heaviest key tiles first
-  const int bh = blockIdx.y;
+  // 1-D grid, key-tile-major: every head's heaviest key tile launches before any
+  // lighter one (longest-processing-time first over the whole grid)
+  const int nbh = p.b * p.heads;
+  const int kt = static_cast<int>(blockIdx.x) / nbh;
+  const int bh = static_cast<int>(blockIdx.x) % nbh;
   const int bi = bh / p.heads, head = bh % p.heads;
   const int qcol = head * D, kcol = p.h + head * D, vcol = 2 * p.h + head * D;
   const int n_it = nq - kt;
@@ -512,7 +515,7 @@ __global__ void __launch_bounds__(512, 1)
     }
   };
   if (warp >= 8 && warp < 12) {
-    regs_dec<104>();
+    regs_dec<120>();
     if (warp == 8 && lane == 0) {
       mbar_arrive_expect_tx(kv_full, 2 * Tile<D>::BYTES);
       tma_tile_rows<D>(smem + L::K, &tm_qkv, kv_full, kcol, bi, kt * AT_TILE, AT_TILE);
@@ -674,7 +677,7 @@ __global__ void __launch_bounds__(512, 1)
     return;
   } else {
     // compute: thread = key row c, query columns [64g, 64g + 64)
-    regs_inc<136>();
+    // (compute warpgroups keep the launch budget of 128 registers)
     const int g = warp >> 2, quad = warp & 3;
     const int c = quad * 32 + lane;
     const int qoff = 64 * g;
@@ -893,7 +896,7 @@ static cudaError_t fused_launch(const void* qkv, int ld_qkv, const void* o, cons
   attn_bwd_pre_kernel<D><<<(tokens + 7) / 8, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(o),
                                                            static_cast<const __nv_bfloat16*>(d_o), ld_o,
                                                            const_cast<float*>(p.delta), p.s, p.b, p.heads);
-  dim3 grid((p.s + AT_TILE - 1) / AT_TILE, p.b * p.heads);
+  const int grid = ((p.s + AT_TILE - 1) / AT_TILE) * p.b * p.heads;
   attn_bwd_fused_kernel<D><<<grid, 512, FusedSmem<D>::TOTAL, st>>>(tq, tdo, tdq, p);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;

@@ -2,7 +2,7 @@
 // Replaces the reference's whole-matrix fp64 attention (P/runtime/mathops.py:83-100):
 //   O = softmax(Q K^T / sqrt(d) + causal mask) V, plus the natural-log LSE per row.
 //
-// CTA = query tiles (2t, 2t+1) of one (batch, head); heaviest pairs first.
+// CTA = query tiles (2t, 2t+1) of one (batch, head); heaviest pairs of all heads first.
 // Two softmax warpgroups (warps 0-3 -> tile A, 4-7 -> tile B) alternate with the
 // tensor core: while group A exponentiates S_A(j), the tensor core runs
 // O_B += P_B(j-1) V(j-1) and S_B(j) = Q_B K(j)^T, and vice versa.
@@ -24,7 +24,7 @@ constexpr int FWD_THREADS = 320;
 #ifdef HX_FWD_TRACE
 __device__ long long g_fwd_trace[8][1024];
 #define HX_TR(slot, idx) \
-  if (blockIdx.x == 0 && blockIdx.y == 0 && (idx) < 1024) g_fwd_trace[slot][idx] = clock64()
+  if (blockIdx.x == 0 && (idx) < 1024) g_fwd_trace[slot][idx] = clock64()
 #else
 #define HX_TR(slot, idx)
 #endif
@@ -62,12 +62,15 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
   const int warp = warp_id(), lane = lane_id();
   const int nq = (p.s + AT_TILE - 1) / AT_TILE;
   const int npairs = (nq + 1) / 2;
-  const int t = npairs - 1 - static_cast<int>(blockIdx.x);
+  // 1-D grid, pair-major: every head's heaviest pair launches before any lighter
+  // one (longest-processing-time first over the whole grid, not per head)
+  const int nbh = p.b * p.heads;
+  const int t = npairs - 1 - static_cast<int>(blockIdx.x) / nbh;
   const int qtile[2] = {2 * t, 2 * t + 1};
   const bool has_b = qtile[1] < nq;
   const int last[2] = {qtile[0], has_b ? qtile[1] : -1};
   const int nkv = has_b ? qtile[1] + 1 : qtile[0] + 1;
-  const int bh = blockIdx.y;
+  const int bh = static_cast<int>(blockIdx.x) % nbh;
   const int bi = bh / p.heads, head = bh % p.heads;
   const int qcol = head * D, kcol = p.h + head * D, vcol = 2 * p.h + head * D;
 
@@ -263,7 +266,7 @@ static cudaError_t fwd_launch(const void* qkv, int ld_qkv, const AttnParams& p, 
     cfg = true;
   }
   const int nq = (p.s + AT_TILE - 1) / AT_TILE;
-  attn_fwd_kernel<D><<<dim3((nq + 1) / 2, p.b * p.heads), FWD_THREADS, FwdSmem<D>::TOTAL, st>>>(tm, p);
+  attn_fwd_kernel<D><<<((nq + 1) / 2) * p.b * p.heads, FWD_THREADS, FwdSmem<D>::TOTAL, st>>>(tm, p);
   return cudaGetLastError();
 }
 

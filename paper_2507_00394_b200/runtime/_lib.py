@@ -70,8 +70,44 @@ def check(rc: int, what: str) -> None:
         raise KernelLibraryError(f"{what} failed: {label}")
 
 
+# Optional per-entry-point device timing (bench.py's in-step roofline): while
+# enabled, every call is bracketed by CUDA events on the current stream, which
+# is the stream every wrapper in kernels.py launches on.
+_timers: dict[str, list] | None = None
+
+
+def start_kernel_timers() -> None:
+    global _timers
+    _timers = {}
+
+
+def stop_kernel_timers() -> dict[str, dict]:
+    """Synchronise and return {entry point: {"launches", "total_ms", "mean_ms"}}."""
+    global _timers
+    import torch
+
+    timers, _timers = _timers or {}, None
+    torch.cuda.synchronize()
+    out = {}
+    for name, evs in timers.items():
+        tot = sum(a.elapsed_time(b) for a, b in evs)
+        out[name] = {"launches": len(evs), "total_ms": tot, "mean_ms": tot / len(evs)}
+    return out
+
+
 def call(name: str, *args) -> None:
-    check(getattr(load(), name)(*args), name)
+    fn = getattr(load(), name)
+    if _timers is None:
+        check(fn(*args), name)
+        return
+    import torch
+
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    rc = fn(*args)
+    b.record()
+    _timers.setdefault(name, []).append((a, b))
+    check(rc, name)
 
 
 def launch_count() -> int:

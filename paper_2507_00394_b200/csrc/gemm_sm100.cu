@@ -67,6 +67,12 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row, int
     for (int j = 0; j < 8; ++j) {
       if (col + 4 * j + 4 > p.N) break;
       float4 w = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      if (epi == HX_EPI_ACC_F32 && p.ksplit > 1) {  // K slices of one tile race: add in L2
+        asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(out + 4 * j), "f"(w.x), "f"(w.y),
+                     "f"(w.z), "f"(w.w)
+                     : "memory");
+        continue;
+      }
       if (epi == HX_EPI_ACC_F32) {
         float4 o = *reinterpret_cast<float4*>(out + 4 * j);
         w.x += o.x; w.y += o.y; w.z += o.z; w.w += o.w;
@@ -318,6 +324,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int num_n = (p.N + BN - 1) / BN;
   const int num_k = (p.K + GEMM_BK - 1) / GEMM_BK;
   const int num_tiles = (num_m / 2) * num_n;
+  // work unit u = (tile u / S, K slice u % S): slices of one tile run on different pairs
+  const int S = p.ksplit;
+  const int num_units = num_tiles * S;
+  auto kslice = [&](int u, int& kb0, int& kb1) {
+    const int ks = u % S;
+    kb0 = ks * num_k / S;
+    kb1 = (ks + 1) * num_k / S;
+  };
   const int first = static_cast<int>(cluster_id_x());
   const int stride = static_cast<int>(nclusters_x());
 
@@ -346,11 +360,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       // ---------------- TMA producer (both CTAs): own A rows + own half of B
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = first; t < num_tiles; t += stride) {
-        int mp, nb;
-        tile_coords(t, num_m / 2, num_n, mp, nb);
+      for (int u = first; u < num_units; u += stride) {
+        int mp, nb, kb0, kb1;
+        tile_coords(u / S, num_m / 2, num_n, mp, nb);
+        kslice(u, kb0, kb1);
         const int m0 = (2 * mp + rank) * GEMM_BM, n0 = nb * BN + rank * 128;
-        for (int kb = 0; kb < num_k; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t bar = mapa_shared(&full[stage], 0);
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * G2_STAGE_BYTES);
@@ -380,12 +395,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = first; t < num_tiles; t += stride, ++it) {
+      for (int u = first; u < num_units; u += stride, ++it) {
         const int acc = it & 1;
+        int kb0, kb1;
+        kslice(u, kb0, kb1);
         mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_k; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * G2_STAGE_BYTES);
@@ -396,7 +413,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                                      : sw128_desc(sa + kk * 32, 16, 1024);
             const uint64_t db = B_MN ? sw128_desc(sb + kk * 2048, 8192, 1024)
                                      : sw128_desc(sb + kk * 32, 16, 1024);
-            umma_f16_ss_2sm(d_tmem, da, db, idesc, (kb | kk) != 0);
+            umma_f16_ss_2sm(d_tmem, da, db, idesc, (kb != kb0) || kk != 0);
           }
           umma_commit_2sm_mc(&empty[stage], 0x3);
           if (++stage == G2_STAGES) { stage = 0; phase ^= 1; }
@@ -409,9 +426,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int sub = warp & 3;
     const uint32_t tempty_leader0 = mapa_shared(&tempty[0], 0);
     int it = 0;
-    for (int t = first; t < num_tiles; t += stride, ++it) {
+    for (int u = first; u < num_units; u += stride, ++it) {
       int mp, nb;
-      tile_coords(t, num_m / 2, num_n, mp, nb);
+      tile_coords(u / S, num_m / 2, num_n, mp, nb);
       const int acc = it & 1;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
@@ -448,7 +465,7 @@ static cudaError_t launch_gemm_2sm(const CUtensorMap& ta, const CUtensorMap& tb,
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  const int pairs = ((p.M + GEMM_BM - 1) / GEMM_BM / 2) * ((p.N + 255) / 256);
+  const int pairs = ((p.M + GEMM_BM - 1) / GEMM_BM / 2) * ((p.N + 255) / 256) * p.ksplit;
   int grid = 2 * (pairs < num_sms / 2 ? pairs : num_sms / 2);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -517,6 +534,29 @@ static int pick_bn(int M, int N, int num_sms) {
   return eff(t128, 1.0) > eff(t256, 1.0) + 0.25 ? 128 : 256;
 }
 
+// K slices per 256 x 256 tile for the pair kernel.  Only fp32-accumulating GEMMs
+// (weight gradients: few tiles, long K) split, and only when the slices fill the
+// pair slots clearly better than whole tiles do; each slice keeps >= 2048 of K.
+// At most 2 slices: measured at GPT-1.3B/32k, 2 slices take the MLP weight
+// gradients (256 tiles on 74 pairs) from 0.81-0.88 to 0.74-0.78 ms, while 3
+// slices (qkv, 192 tiles) were 4% and 8 slices (o, 64 tiles) 26% slower than
+// none: the red.global traffic then outweighs the better wave fill.
+// HX_GEMM_KSPLIT=n forces n (1 disables), for A/B runs.
+static int pick_ksplit(const GemmParams& p, int tiles, int slots) {
+  static const int forced = getenv("HX_GEMM_KSPLIT") ? atoi(getenv("HX_GEMM_KSPLIT")) : 0;
+  if (p.epi != HX_EPI_ACC_F32) return 1;
+  if (forced > 0) return forced;
+  auto eff = [&](int s) {
+    const long units = static_cast<long>(tiles) * s;
+    const long waves = (units + slots - 1) / slots;
+    return static_cast<double>(units) / static_cast<double>(waves * slots);
+  };
+  int best = 1;
+  for (int s = 2; s <= 2 && p.K / s >= 2048; ++s)
+    if (eff(s) > eff(best) + 0.05) best = s;
+  return best;
+}
+
 cudaError_t gemm_launch(const GemmOperand& a, const GemmOperand& b, const GemmParams& p,
                         cudaStream_t stream) {
   const int num_sms = hx::num_sms();  // persistent grid size (honours HX_SM_RESERVE)
@@ -537,11 +577,13 @@ cudaError_t gemm_launch(const GemmOperand& a, const GemmOperand& b, const GemmPa
   // cta_group::2 also wins with fewer tiles than pairs of SMs (e.g. the 2048 x 2048
   // weight gradient: 64 pairs); only tiny GEMMs stay on single CTAs
   if (cl_mode == 2 && num_m % 2 == 0 && p.N > 128 && pairs >= 32) {
+    GemmParams q = p;
+    q.ksplit = pick_ksplit(p, pairs, num_sms / 2);
     e = b.mn ? make_tma_2d(&tb, b.ptr, p.K, p.N, b.ld, 64, 64) : make_tma_2d(&tb, b.ptr, p.N, p.K, b.ld, 64, 128);
     if (e != cudaSuccess) return e;
-    if (a.mn && b.mn) return launch_gemm_2sm<true, true>(ta, tb, p, num_sms, stream);
-    if (!a.mn && b.mn) return launch_gemm_2sm<false, true>(ta, tb, p, num_sms, stream);
-    if (!a.mn && !b.mn) return launch_gemm_2sm<false, false>(ta, tb, p, num_sms, stream);
+    if (a.mn && b.mn) return launch_gemm_2sm<true, true>(ta, tb, q, num_sms, stream);
+    if (!a.mn && b.mn) return launch_gemm_2sm<false, true>(ta, tb, q, num_sms, stream);
+    if (!a.mn && !b.mn) return launch_gemm_2sm<false, false>(ta, tb, q, num_sms, stream);
     return cudaErrorNotSupported;
   }
   e = b.mn ? make_tma_2d(&tb, b.ptr, p.K, p.N, b.ld, 64, 64)

@@ -60,6 +60,18 @@ def test_gemm_dw_layout_accumulates(M, N, Kd):
     assert rel_err(acc, want) < 1e-4
 
 
+@pytest.mark.parametrize("M,N,Kd", [(2048, 8192, 8192), (4096, 4000, 12008)])
+def test_gemm_dw_split_k(M, N, Kd):
+    # long-K weight gradients with 256 tiles on 74 pairs take the 2-slice pair
+    # kernel (slices added into acc with red.global.add); ragged N and K
+    x, dy = rnd(Kd, M, seed=15), rnd(Kd, N, seed=16)
+    acc = torch.randn(M, N, device=DEV)
+    want = acc + x.float().t() @ dy.float()
+    K.linear_dw(x, dy, acc, accumulate=True)
+    torch.cuda.synchronize()
+    assert rel_err(acc, want) < 1e-4
+
+
 def test_gemm_epilogues():
     T, Kd, N = 512, 256, 1024
     x, w = rnd(T, Kd, seed=7), rnd(Kd, N, scale=Kd ** -0.5, seed=8)

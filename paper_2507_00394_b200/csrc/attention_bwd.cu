@@ -480,11 +480,10 @@ __global__ void __launch_bounds__(512, 1)
 
   const int warp = warp_id(), lane = lane_id();
   const int nq = (p.s + AT_TILE - 1) / AT_TILE;
-  // 1-D grid, key-tile-major: every head's heaviest key tile launches before any
-  // lighter one (longest-processing-time first over the whole grid)
-  const int nbh = p.b * p.heads;
-  const int kt = static_cast<int>(blockIdx.x) / nbh;
-  const int bh = static_cast<int>(blockIdx.x) % nbh;
+  // 1-D grid in bands of (batch, head)s, key-tile-major inside a band: heaviest
+  // key tiles first (attention_common.cuh band_order)
+  int bh, kt;
+  band_order(static_cast<int>(blockIdx.x), nq, p.b * p.heads, bh, kt);
   const int bi = bh / p.heads, head = bh % p.heads;
   const int qcol = head * D, kcol = p.h + head * D, vcol = 2 * p.h + head * D;
   const int n_it = nq - kt;

@@ -51,6 +51,25 @@ HX_DEVICE void tma_tile_rows(void* dst, const CUtensorMap* map, uint64_t* bar, i
     tma_load_3d(static_cast<uint8_t*>(dst) + a * rows * 128, map, bar, col0 + 64 * a, bi, s0);
 }
 
+// CTA order of the attention grids: blocks enumerate bands of `band` (batch, head)
+// pairs; inside a band the work index w (0 = heaviest) is the slow coordinate, so
+// every head of the band starts its heaviest tile before any lighter one.
+// Default 0 = one band over all heads (global longest-first).  Measured at
+// GPT-1.3B/32k against per-head order: forward +6%, backward +4%; bands of 8 / 4
+// heads (more K/V reuse in L2, 5x less forward DRAM traffic) were 1.4% / 3.5%
+// slower on the backward and neutral on the forward.
+#ifndef HX_ATTN_BAND
+#define HX_ATTN_BAND 0
+#endif
+HX_DEVICE void band_order(int blk, int nwork, int nbh, int& bh, int& w) {
+  const int band = (HX_ATTN_BAND > 0 && HX_ATTN_BAND < nbh) ? HX_ATTN_BAND : nbh;
+  const int b0 = blk / (band * nwork) * band;
+  const int r = blk - b0 * nwork;
+  const int bsz = min(band, nbh - b0);
+  w = r / bsz;
+  bh = b0 + r % bsz;
+}
+
 HX_DEVICE float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

@@ -62,15 +62,16 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
   const int warp = warp_id(), lane = lane_id();
   const int nq = (p.s + AT_TILE - 1) / AT_TILE;
   const int npairs = (nq + 1) / 2;
-  // 1-D grid, pair-major: every head's heaviest pair launches before any lighter
-  // one (longest-processing-time first over the whole grid, not per head)
-  const int nbh = p.b * p.heads;
-  const int t = npairs - 1 - static_cast<int>(blockIdx.x) / nbh;
+  // 1-D grid in bands of HX_ATTN_BAND (batch, head)s; inside a band, pair-major:
+  // each head's heaviest pair launches before any lighter one (longest-processing-
+  // time first), while the band keeps the concurrently streamed K/V in L2
+  int bh, t;
+  band_order(static_cast<int>(blockIdx.x), npairs, p.b * p.heads, bh, t);
+  t = npairs - 1 - t;
   const int qtile[2] = {2 * t, 2 * t + 1};
   const bool has_b = qtile[1] < nq;
   const int last[2] = {qtile[0], has_b ? qtile[1] : -1};
   const int nkv = has_b ? qtile[1] + 1 : qtile[0] + 1;
-  const int bh = static_cast<int>(blockIdx.x) % nbh;
   const int bi = bh / p.heads, head = bh % p.heads;
   const int qcol = head * D, kcol = p.h + head * D, vcol = 2 * p.h + head * D;
 

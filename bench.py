@@ -242,7 +242,8 @@ def main() -> None:
     from paper_2507_00394_b200.runtime import _lib, kernels as K
     from paper_2507_00394_b200.runtime.executor import DeviceModel, make_pair_groups, stage_fields
     from paper_2507_00394_b200.runtime.model import DeviceLayer, random_device_layer
-    from paper_2507_00394_b200.simulate import measured_durations, metrics_from_timeline, predict_pipeline, simulate
+    from paper_2507_00394_b200.simulate import (measured_durations, metrics_from_timeline, overlap_report,
+                                                predict_pipeline, simulate)
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -352,6 +353,12 @@ def main() -> None:
         sim = simulate(sched, table)
         predicted = {"bubble_fraction": sim.metrics.bubble_fraction,
                      "makespan_ms": sim.metrics.makespan / 1e6, "measured_makespan_ms": measured.makespan}
+        if world > 1:
+            # P/simulate.py:118-151 on the measured timeline: transfer waits, and the part the
+            # two-fold order should have hidden (rank clocks start at each rank's run start)
+            ov = overlap_report(sched, tl)
+            predicted["measured_comm_wait_ms"] = ov.total_wait
+            predicted["measured_steady_comm_wait_ms"] = ov.steady_wait
         if world == 1:
             # helix vs same-kernel 1F1B at p = 2/4/8 predicted from these measured component
             # times (reference simulator, NVLink 770 GB/s per direction): a prediction only

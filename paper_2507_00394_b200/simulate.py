@@ -21,7 +21,8 @@ from dataclasses import dataclass
 
 from .costs import DurationTable
 from .engine import CommModel, make_duration_fn, replay
-from .schedule import SEND, Schedule
+from .generators import comm_hidden, warmup_mbs
+from .schedule import RECV, SEND, Schedule
 
 
 @dataclass
@@ -118,9 +119,12 @@ def predict_pipeline(cfg, durations: DurationTable, stages=(2, 4, 8), link_gbs: 
         for method in methods:
             res = simulate(generate(method, c, durations), durations, comm)
             tokens = c.m * c.s * c.b
+            ov = overlap_report(res)
             row[method] = {"tokens_per_s": tokens / (res.metrics.makespan * 1e-9),
                            "bubble_fraction": res.metrics.bubble_fraction,
-                           "makespan_ms": res.metrics.makespan / 1e6}
+                           "makespan_ms": res.metrics.makespan / 1e6,
+                           # transfer waits: all, and those the schedule meant to hide
+                           "comm_wait_ms": ov.total_wait / 1e6, "steady_comm_wait_ms": ov.steady_wait / 1e6}
         if "1f1b" in row:
             for method in methods:
                 if method != "1f1b":
@@ -140,6 +144,69 @@ def simulate(sched: Schedule, durations: DurationTable, comm: CommModel | None =
     res = replay(sched, make_duration_fn(durations, fused, chunk_rc), comm or CommModel.zero())
     return SimResult(sched, res.timeline,
                      metrics_from_timeline(sched, res.timeline, durations.time_unit))
+
+
+# --- communication-wait accounting (``P/simulate.py:100-151``) ----------------------------
+
+
+@dataclass
+class OverlapRow:
+    task_id: str
+    stage: int
+    mb: int
+    wait: float
+    hidden: bool          # the schedule expects this task's inbound transfer to be hidden
+
+
+@dataclass
+class OverlapReport:
+    rows: list[OverlapRow]
+    per_stage_wait: list[float]
+    total_wait: float
+    steady_wait: float    # waits on tasks whose transfers should have been hidden
+    warmup_mbs: set[int]
+
+
+def overlap_report(sched_or_result, timeline=None) -> OverlapReport:
+    """How long each compute task started after it could have (its stage free
+    and every producer finished), on a simulated or device-measured timeline.
+
+    A task's floor is the end of the previous task on its stage and of each
+    dependency; a RECV dependency is charged at its payload's producer finish,
+    so the wait beyond the floor is wire / queueing time.  Two-fold schedules
+    expect the second member of each micro-batch pair to hide its transfer
+    (``comm_hidden``); other schedules expect every micro-batch after the
+    warm-up to.  ``steady_wait`` sums the waits of those tasks: the part of the
+    communication the schedule failed to hide.  Accepts ``overlap_report(result)``
+    (a :class:`SimResult`, as the reference) or ``overlap_report(sched, timeline)``.
+    """
+    if timeline is None:
+        sched, tl = sched_or_result.sched, sched_or_result.timeline
+    else:
+        sched, tl = sched_or_result, timeline
+    p = int(sched.meta["p"])
+    twofold = int(sched.meta.get("fold", 1)) == 2
+    warm = warmup_mbs(sched)
+    rows: list[OverlapRow] = []
+    per_stage = [0] * sched.n_stages
+    for st, order in enumerate(sched.per_stage_order):
+        stage_free = 0
+        for tid in order:
+            task = sched.tasks[tid]
+            ready = stage_free
+            for dep in task.deps:
+                d = sched.tasks[dep]
+                # RECV -> its SEND -> the compute task that produced the payload
+                src = sched.tasks[d.deps[0]].deps[0] if d.kind == RECV else dep
+                ready = max(ready, tl[src][1])
+            start, end = tl[tid]
+            if start > ready:
+                hidden = comm_hidden(task.kind, task.mb, p) if twofold else task.mb not in warm
+                rows.append(OverlapRow(tid, st, task.mb, start - ready, hidden))
+                per_stage[st] += start - ready
+            stage_free = end
+    return OverlapReport(rows, per_stage, sum(per_stage),
+                         sum(r.wait for r in rows if r.hidden), warm)
 
 
 # --- exports (reference schema, ``P/simulate.py:157-196``) -------------------------------

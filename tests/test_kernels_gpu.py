@@ -133,7 +133,9 @@ def attn_ref(qkv, s, b, heads):
     return o.permute(2, 0, 1, 3).reshape(s * b, h), lse
 
 
-ATTN_CASES = [(256, 1, 2, 64), (384, 1, 2, 128), (200, 2, 2, 64), (1024, 1, 4, 128), (130, 1, 1, 128)]
+ATTN_CASES = [(256, 1, 2, 64), (384, 1, 2, 128), (200, 2, 2, 64), (1024, 1, 4, 128), (130, 1, 1, 128),
+              # multi-head 1-D grids in longest-first order, ragged tails
+              (2048, 2, 3, 128), (1000, 1, 8, 64)]
 
 
 @pytest.mark.parametrize("s,b,heads,d", ATTN_CASES)

@@ -480,10 +480,10 @@ __global__ void __launch_bounds__(512, 1)
 
   const int warp = warp_id(), lane = lane_id();
   const int nq = (p.s + AT_TILE - 1) / AT_TILE;
-  // 1-D grid in bands of (batch, head)s, key-tile-major inside a band: heaviest
-  // key tiles first (attention_common.cuh band_order)
+  // 1-D grid in bands of p.band (batch, head)s, key-tile-major inside a band:
+  // heaviest key tiles first (attention_common.cuh band_order)
   int bh, kt;
-  band_order(static_cast<int>(blockIdx.x), nq, p.b * p.heads, bh, kt);
+  band_order(static_cast<int>(blockIdx.x), nq, p.b * p.heads, p.band, bh, kt);
   const int bi = bh / p.heads, head = bh % p.heads;
   const int qcol = head * D, kcol = p.h + head * D, vcol = 2 * p.h + head * D;
   const int n_it = nq - kt;
@@ -914,6 +914,13 @@ cudaError_t attn_bwd_launch(const void* qkv, int ld_qkv, const void* o, const vo
   p.h = heads * d;
   p.scale = 1.0f / sqrtf(static_cast<float>(d));
   p.scale_log2 = p.scale * LOG2E;
+  // Backward band: one head at a time (its fp32 dQ accumulator, s * d * 4 bytes,
+  // and Q / dO stay in L2).  In the GPT-1.3B/32k bench step: 10.45-10.47 ms per
+  // call with 1 head, 10.54 with 4, 10.64-10.66 with 8, 10.79-10.80 with all 16
+  // (9x the DRAM traffic of 1 head: 11.9 GB per call, and lower clocks under the
+  // power cap), although all 16 measured 4% faster in isolation.
+  static const int forced_band = getenv("HX_ATTN_BWD_BAND") ? atoi(getenv("HX_ATTN_BWD_BAND")) : 0;
+  p.band = forced_band > 0 ? forced_band : 1;
   p.lse = const_cast<float*>(lse);
   p.delta = delta;
   p.dqkv = static_cast<__nv_bfloat16*>(dqkv);

@@ -32,6 +32,7 @@ struct AttnParams {
   const float* delta;  // [b, heads, s], rowsum(dO * O)
   __nv_bfloat16* dqkv;
   int ld_dqkv;
+  int band;            // (batch, head)s per band of the CTA order (band_order)
 };
 
 // Smem descriptors for K-step kk (16 elements) of a tile with `rows` rows.
@@ -53,16 +54,12 @@ HX_DEVICE void tma_tile_rows(void* dst, const CUtensorMap* map, uint64_t* bar, i
 
 // CTA order of the attention grids: blocks enumerate bands of `band` (batch, head)
 // pairs; inside a band the work index w (0 = heaviest) is the slow coordinate, so
-// every head of the band starts its heaviest tile before any lighter one.
-// Default 0 = one band over all heads (global longest-first).  Measured at
-// GPT-1.3B/32k against per-head order: forward +6%, backward +4%; bands of 8 / 4
-// heads (more K/V reuse in L2, 5x less forward DRAM traffic) were 1.4% / 3.5%
-// slower on the backward and neutral on the forward.
-#ifndef HX_ATTN_BAND
-#define HX_ATTN_BAND 0
-#endif
-HX_DEVICE void band_order(int blk, int nwork, int nbh, int& bh, int& w) {
-  const int band = (HX_ATTN_BAND > 0 && HX_ATTN_BAND < nbh) ? HX_ATTN_BAND : nbh;
+// every head of the band starts its heaviest tile before any lighter one.  Wide
+// bands shorten the grid's tail; narrow bands keep the concurrently streamed
+// per-head data (K/V, the fp32 dQ accumulator) in L2.  Under the B200's power
+// cap the DRAM traffic costs clock: see attn_band() in the launchers.
+HX_DEVICE void band_order(int blk, int nwork, int nbh, int band, int& bh, int& w) {
+  band = band < 1 ? 1 : (band > nbh ? nbh : band);
   const int b0 = blk / (band * nwork) * band;
   const int r = blk - b0 * nwork;
   const int bsz = min(band, nbh - b0);

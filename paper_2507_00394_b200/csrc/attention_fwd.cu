@@ -62,11 +62,11 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
   const int warp = warp_id(), lane = lane_id();
   const int nq = (p.s + AT_TILE - 1) / AT_TILE;
   const int npairs = (nq + 1) / 2;
-  // 1-D grid in bands of HX_ATTN_BAND (batch, head)s; inside a band, pair-major:
-  // each head's heaviest pair launches before any lighter one (longest-processing-
-  // time first), while the band keeps the concurrently streamed K/V in L2
+  // 1-D grid in bands of p.band (batch, head)s; inside a band, pair-major: each
+  // head's heaviest pair launches before any lighter one (longest-processing-time
+  // first), while the band keeps the concurrently streamed K/V in L2
   int bh, t;
-  band_order(static_cast<int>(blockIdx.x), npairs, p.b * p.heads, bh, t);
+  band_order(static_cast<int>(blockIdx.x), npairs, p.b * p.heads, p.band, bh, t);
   t = npairs - 1 - t;
   const int qtile[2] = {2 * t, 2 * t + 1};
   const bool has_b = qtile[1] < nq;
@@ -280,6 +280,17 @@ cudaError_t attn_fwd_launch(const void* qkv, int ld_qkv, void* o, int ld_o, floa
   p.h = heads * d;
   p.scale = 1.0f / sqrtf(static_cast<float>(d));
   p.scale_log2 = p.scale * LOG2E;
+  // Forward band: as many heads as keep their K/V (2 * s * d bf16 each) within
+  // ~64 MB of L2.  In the GPT-1.3B/32k bench step (1.3B: 16 MB per head) bands of
+  // 4 heads ran the forward in 4.31-4.34 ms against 4.38-4.40 (1 head) and
+  // 4.40-4.47 (all 16 heads, 5x the DRAM reads; lower clocks under the power cap).
+  {
+    const int64_t per_head = 2LL * s * d * 2;
+    int band = static_cast<int>((64LL << 20) / (per_head > 0 ? per_head : 1));
+    static const int forced = getenv("HX_ATTN_FWD_BAND") ? atoi(getenv("HX_ATTN_FWD_BAND")) : 0;
+    if (forced > 0) band = forced;
+    p.band = band < 1 ? 1 : band;
+  }
   p.o = static_cast<__nv_bfloat16*>(o);
   p.ld_o = ld_o;
   p.lse = lse;

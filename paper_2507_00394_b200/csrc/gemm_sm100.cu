@@ -43,11 +43,12 @@ struct GemmCfg {
   static constexpr int TMEM_COLS = 2 * BN;
 };
 
-__device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb, int& nb) {
-  const int per_group = GEMM_GROUP_M * num_n;
+__device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb, int& nb,
+                                            int group_m = GEMM_GROUP_M) {
+  const int per_group = group_m * num_n;
   const int group = t / per_group;
-  const int first_m = group * GEMM_GROUP_M;
-  const int gm = min(num_m - first_m, GEMM_GROUP_M);
+  const int first_m = group * group_m;
+  const int gm = min(num_m - first_m, group_m);
   const int r = t - group * per_group;
   mb = first_m + r % gm;
   nb = r / gm;
@@ -362,7 +363,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       uint32_t phase = 0;
       for (int u = first; u < num_units; u += stride) {
         int mp, nb, kb0, kb1;
-        tile_coords(u / S, num_m / 2, num_n, mp, nb);
+        tile_coords(u / S, num_m / 2, num_n, mp, nb, p.group_m);
         kslice(u, kb0, kb1);
         const int m0 = (2 * mp + rank) * GEMM_BM, n0 = nb * BN + rank * 128;
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -428,7 +429,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     int it = 0;
     for (int u = first; u < num_units; u += stride, ++it) {
       int mp, nb;
-      tile_coords(u / S, num_m / 2, num_n, mp, nb);
+      tile_coords(u / S, num_m / 2, num_n, mp, nb, p.group_m);
       const int acc = it & 1;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
@@ -557,6 +558,42 @@ static int pick_ksplit(const GemmParams& p, int tiles, int slots) {
   return best;
 }
 
+// Tile raster of the pair kernel: pair-rows per M-group (M fastest inside a
+// group, groups in order).  Picked to minimise the modelled DRAM bytes of the
+// operand panels: a wave of `conc` concurrent tiles re-reads A panels once per
+// n-column wave unless the group's A panels stay in L2, and B panels once per
+// group unless all of B stays in L2.  Narrow-N GEMMs (N = 2048: 8 tile columns)
+// then run whole tile rows per wave (A read once) instead of 16-row groups that
+// read A 1.7x; wide-N weight gradients keep the tall groups.
+// HX_GEMM_GROUP=n forces n, for A/B runs.
+static int pick_group(const GemmParams& p, int num_mp, int num_n, int conc) {
+  static const int forced = getenv("HX_GEMM_GROUP") ? atoi(getenv("HX_GEMM_GROUP")) : 0;
+  if (forced > 0) return forced;
+  const double budget = 16.0 * (1 << 20);  // L2 bytes a group's panels may hold across waves
+  const double a_panel = 256.0 * p.K * 2, b_panel = 256.0 * p.K * 2;
+  const double a_total = a_panel * num_mp, b_total = b_panel * num_n;
+  double best_bytes = 0;
+  int best = GEMM_GROUP_M;
+  for (int g : {GEMM_GROUP_M, 8, 4, 2, 1}) {
+    double a_rd, b_rd;
+    if (conc >= g * num_n) {  // a wave covers whole tile rows
+      const double m_conc = static_cast<double>(conc) / num_n;
+      a_rd = a_total;
+      b_rd = b_total <= budget ? b_total : b_total * num_mp / m_conc;
+    } else {
+      const int m_conc = g < num_mp ? g : num_mp;
+      const double n_conc = static_cast<double>(conc) / m_conc;
+      a_rd = m_conc * a_panel <= budget ? a_total : a_total * num_n / n_conc;
+      b_rd = b_total <= budget ? b_total : b_total * ((num_mp + g - 1) / g);
+    }
+    if (g == GEMM_GROUP_M || a_rd + b_rd < 0.95 * best_bytes) {
+      best_bytes = a_rd + b_rd;
+      best = g;
+    }
+  }
+  return best;
+}
+
 cudaError_t gemm_launch(const GemmOperand& a, const GemmOperand& b, const GemmParams& p,
                         cudaStream_t stream) {
   const int num_sms = hx::num_sms();  // persistent grid size (honours HX_SM_RESERVE)
@@ -579,6 +616,7 @@ cudaError_t gemm_launch(const GemmOperand& a, const GemmOperand& b, const GemmPa
   if (cl_mode == 2 && num_m % 2 == 0 && p.N > 128 && pairs >= 32) {
     GemmParams q = p;
     q.ksplit = pick_ksplit(p, pairs, num_sms / 2);
+    q.group_m = pick_group(p, num_m / 2, (p.N + 255) / 256, (num_sms / 2) / q.ksplit);
     e = b.mn ? make_tma_2d(&tb, b.ptr, p.K, p.N, b.ld, 64, 64) : make_tma_2d(&tb, b.ptr, p.N, p.K, b.ld, 64, 128);
     if (e != cudaSuccess) return e;
     if (a.mn && b.mn) return launch_gemm_2sm<true, true>(ta, tb, q, num_sms, stream);

@@ -118,7 +118,7 @@ int hx_gemm(const void* A, int lda, int a_mn, const void* B, int ldb, int b_mn, 
   if (!b_mn && ldb < K) return HX_E_SHAPE;
   if (b_mn && ldb < N) return HX_E_SHAPE;
   GemmOperand a{A, lda, a_mn != 0}, b{B, ldb, b_mn != 0};
-  GemmParams p{M, N, K, epi, C, ldc, aux, ld_aux, out2, ld_out2, 1};
+  GemmParams p{M, N, K, epi, C, ldc, aux, ld_aux, out2, ld_out2, 1, 16};
   return ret(gemm_launch(a, b, p, as_stream(stream)), 1);
 }
 

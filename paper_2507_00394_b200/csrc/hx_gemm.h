@@ -25,6 +25,7 @@ struct GemmParams {
   void* out2;            // bf16 [M, N]: GeLU output (GELU)
   int ldo2;
   int ksplit;            // K slices per tile (pair kernel, ACC_F32 only; set by gemm_launch)
+  int group_m;           // tile-raster M-group in pair-rows (pair kernel; set by gemm_launch)
 };
 
 // 2-D bf16 tensor map over a row-major [rows, cols] matrix with row stride ld,

@@ -95,9 +95,11 @@ def test_gemm_epilogues():
     assert rel_err(dm, (dy.float() @ w2.float().t()) * gelu_grad) < 1e-2
 
 
-@pytest.mark.parametrize("h", [256, 2048, 4096])
-def test_layernorm_fwd_bwd(h):
-    T = 1000
+@pytest.mark.parametrize("T,h,with_res", [(1000, 256, True), (1001, 2048, True), (1003, 2048, False),
+                                           (999, 4096, True), (517, 8192, True), (300, 264, False)])
+def test_layernorm_fwd_bwd(T, h, with_res):
+    # ragged row counts, h up to 8192 and h % 256 != 0, with and without the
+    # residual gradient; dgain / dbias accumulate into their prior contents
     x = rnd(T, h, seed=13) * 2 + 0.5
     gain = (1 + 0.1 * torch.randn(h, device=DEV))
     bias = 0.1 * torch.randn(h, device=DEV)
@@ -105,18 +107,19 @@ def test_layernorm_fwd_bwd(h):
     xf = x.float().requires_grad_(True)
     ref = torch.nn.functional.layer_norm(xf, (h,), gain, bias, eps=1e-5)
     dy = rnd(T, h, seed=14)
-    dres = rnd(T, h, seed=15)
-    dg = torch.zeros(h, device=DEV)
-    db = torch.zeros(h, device=DEV)
+    dres = rnd(T, h, seed=15) if with_res else None
+    dg0, db0 = torch.randn(h, device=DEV), torch.randn(h, device=DEV)
+    dg, db = dg0.clone(), db0.clone()
     dx = torch.empty_like(x)
     K.layernorm_bwd(dy, x, gain, dres, dx, dg, db)
     torch.cuda.synchronize()
     assert rel_err(y, ref) < 1e-2
     (gx,) = torch.autograd.grad(ref, xf, dy.float())
     xhat = (xf - xf.mean(-1, keepdim=True)) / torch.sqrt(xf.var(-1, unbiased=False, keepdim=True) + 1e-5)
-    assert rel_err(dx, gx + dres.float()) < 2e-2
-    assert rel_err(dg, (dy.float() * xhat).sum(0)) < 1e-3
-    assert rel_err(db, dy.float().sum(0)) < 1e-3
+    want_dx = gx + dres.float() if with_res else gx
+    assert rel_err(dx, want_dx) < 2e-2
+    assert rel_err(dg - dg0, (dy.float() * xhat).sum(0)) < 1e-3
+    assert rel_err(db - db0, dy.float().sum(0)) < 1e-3
 
 
 def attn_ref(qkv, s, b, heads):

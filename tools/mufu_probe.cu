@@ -100,6 +100,38 @@ __global__ void k_ex2_f2fp(float* out, float seed) {
   if (s == 12345.f) out[0] = s;
 }
 
+// packed exponentials: two results per MUFU instruction if the unit is 2-wide
+__device__ __forceinline__ uint32_t ex2_f16x2(uint32_t x) {
+  uint32_t y;
+  asm volatile("ex2.approx.f16x2 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t ex2_bf16x2(uint32_t x) {
+  uint32_t y;
+  asm volatile("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+__global__ void k_ex2_f16x2(float* out, float seed) {
+  uint32_t v[CH];
+  for (int c = 0; c < CH; ++c) v[c] = 0xb800b800u + threadIdx.x + c;  // ~ -0.5 halves
+  for (int i = 0; i < ITERS; ++i)
+#pragma unroll
+    for (int c = 0; c < CH; ++c) v[c] = ex2_f16x2(v[c]) ^ 0x80008000u;
+  uint32_t s = 0;
+  for (int c = 0; c < CH; ++c) s ^= v[c];
+  if (s == 12345) out[0] = 1;
+}
+__global__ void k_ex2_bf16x2(float* out, float seed) {
+  uint32_t v[CH];
+  for (int c = 0; c < CH; ++c) v[c] = 0xbf00bf00u + threadIdx.x + c;
+  for (int i = 0; i < ITERS; ++i)
+#pragma unroll
+    for (int c = 0; c < CH; ++c) v[c] = ex2_bf16x2(v[c]) ^ 0x80008000u;
+  uint32_t s = 0;
+  for (int c = 0; c < CH; ++c) s ^= v[c];
+  if (s == 12345) out[0] = 1;
+}
+
 int main() {
   int dev = 0, sms = 0, clk = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -130,6 +162,8 @@ int main() {
   run("f2fp_bf16x2", k_f2fp, 1.0);
   run("alu_bf16x2", k_alupack, 1.0);
   run("ex2+f2fp (pairs)", k_ex2_f2fp, 1.0);
+  run("ex2_f16x2 (elements)", k_ex2_f16x2, 2.0);
+  run("ex2_bf16x2 (elements)", k_ex2_bf16x2, 2.0);
   printf("{\"sms\": %d, \"max_clock_mhz\": %d, \"err\": \"%s\"}\n", sms, clk / 1000,
          cudaGetErrorString(cudaGetLastError()));
   return 0;

@@ -11,13 +11,17 @@
 //   O += P V     TS-MMA (A = P from TMEM, B = V MN-major from smem) -> TMEM O_g
 // O is rescaled only when a row's running max grows by more than 2^8 (exponents
 // stay <= 256, exact in fp32), so rescales are rare after the first tiles.
-// Warp 8 issues TMA (Q once, K/V through a 5-slot ring), warp 9 issues MMAs and owns TMEM.
+// Warp 8 issues TMA (Q once, K/V through a 5-slot ring), warp 9 issues MMAs and owns TMEM;
+// warps 10-11 idle (they complete warpgroup 2 for setmaxnreg).
 // TMEM (512 columns): S_A 0-127 | S_B 128-255 | O_A 256-383 | O_B 384-511.
 #include "attention_common.cuh"
 
 namespace hx {
 
-constexpr int FWD_THREADS = 320;
+// 12 warps = 3 warpgroups: softmax WG0 / WG1, and WG2 = TMA (warp 8), MMA (warp
+// 9), two idle warps (10, 11) so that setmaxnreg can move registers from WG2 to
+// the softmax warpgroups (the instruction acts on whole warpgroups).
+constexpr int FWD_THREADS = 384;
 
 // Debug build only (-DHX_FWD_TRACE): clock64 stamps of CTA (0,0)'s pipeline
 // events, read back with hx_debug_fwd_trace (tools/fwd_trace.py).
@@ -28,6 +32,11 @@ __device__ long long g_fwd_trace[8][1024];
 #else
 #define HX_TR(slot, idx)
 #endif
+
+// setmaxnreg budgets: 2 x 128 x 216 + 128 x 72 = 64 K registers.  The launch
+// budget is 168 (65536 / 384, rounded down to 8).
+constexpr int FWD_REGS_SOFTMAX = 216;
+constexpr int FWD_REGS_ISSUE = 72;
 
 template <int D>
 struct FwdSmem {
@@ -88,6 +97,18 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
   // ring slot n: K(n/2) for even n, V(n/2) for odd n
   auto slot_addr = [&](int n) { return smem + L::KV + (n % NS) * Tile<D>::BYTES; };
 
+  // Each role ends the kernel itself (no code shared after the role branches,
+  // so ptxas allocates each under its own setmaxnreg budget).
+  auto finish = [&]() {
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 9) {
+      tc_fence_after();
+      tmem_dealloc(tmem, 512);
+    }
+  };
+  if (warp >= 8) {
+  regs_dec<FWD_REGS_ISSUE>();
   if (warp == 8) {
     if (lane == 0) {  // ---------------- TMA producer
       mbar_arrive_expect_tx(q_full, (has_b ? 2 : 1) * Tile<D>::BYTES);
@@ -158,7 +179,12 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       umma_commit(&o_full[0]);
       umma_commit(&o_full[1]);
     }
-  } else {
+  }
+  finish();
+  return;
+  }
+  regs_inc<FWD_REGS_SOFTMAX>();
+  {
     // ---------------- softmax warpgroups: thread = query row of tile g
     const int g = warp >> 2;
     const int quad = warp & 3;
@@ -185,49 +211,88 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
           for (int i = 0; i < AT_TILE; ++i)
             if (i > r) raw[i] = __float_as_uint(-INFINITY);
         }
+        // P = 2^(s*c - m) as bf16 over the first 64 columns of S; returns the row sum.
+        // Packed pairs (FFMA2), row sum on packed pairs (FADD2).
+        auto write_p = [&](float m) {
+          const uint64_t c2 = f2pack(c, c), nm2 = f2pack(-m, -m);
+          uint64_t rs2[2] = {f2pack(0.f, 0.f), f2pack(0.f, 0.f)};
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            uint32_t pk[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const uint64_t x2 = ffma2(f2pack(__uint_as_float(raw[half * 64 + 2 * i]),
+                                               __uint_as_float(raw[half * 64 + 2 * i + 1])), c2, nm2);
+              float e0, e1;
+              pk[i] = exp2_pack_mixed(x2, i, e0, e1);
+              rs2[i & 1] = fadd2(rs2[i & 1], f2pack(e0, e1));
+            }
+            tmem_st32(tS + half * 32, pk);
+          }
+          const float2 ra = f2unpack(rs2[0]), rb = f2unpack(rs2[1]);
+          return (ra.x + ra.y) + (rb.x + rb.y);
+        };
         // row max: four independent 3-input-max chains
-        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        auto row_max = [&]() {
+          float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-        for (int i = 0; i < AT_TILE; i += 8)
+          for (int i = 0; i < AT_TILE; i += 8)
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            m4[k] = fmax3(m4[k], __uint_as_float(raw[i + 2 * k]), __uint_as_float(raw[i + 2 * k + 1]));
-        float mx = fmax3(m4[0], m4[1], fmaxf(m4[2], m4[3])) * c;
-        const float m_new = (mx > m_used + 8.0f) ? mx : m_used;
-        const float alpha = fast_exp2(m_used - m_new);
-        if (j > 0 && __any_sync(0xffffffffu, m_new != m_used)) {
-          // O_g holds PV(j-1): complete, since S_g(j) was issued after it
+            for (int k = 0; k < 4; ++k)
+              m4[k] = fmax3(m4[k], __uint_as_float(raw[i + 2 * k]), __uint_as_float(raw[i + 2 * k + 1]));
+          return fmax3(m4[0], m4[1], fmaxf(m4[2], m4[3])) * c;
+        };
+        // Speculative exponentials (j > 0): P is computed against the running max
+        // m_used while the tile's max is reduced alongside (independent
+        // instructions, free issue slots next to the MUFU-bound exps), so the max
+        // reduction leaves the softmax -> PV -> S chain.  Only when some row's max
+        // grew by more than 2^8 does the warp redo the tile: rescale O, recompute P.
+        float rowsum = 0.f;
+        float mx = -INFINITY;
+        bool redo = true;
+        if (j > 0) {
+          rowsum = write_p(m_used);
+          mx = row_max();
+          redo = __any_sync(0xffffffffu, mx > m_used + 8.0f);
+        } else {
+          mx = row_max();
+        }
+        float alpha = 1.f;
+        if (redo) {
+          const float m_new = (mx > m_used + 8.0f) ? mx : m_used;
+          alpha = fast_exp2(m_used - m_new);
+          if (j > 0) {
+            tmem_wait_st();  // the speculative P stores land before being overwritten
+            // O_g holds PV(j-1): complete, since S_g(j) was issued after it
 #pragma unroll
-          for (int ch = 0; ch < D / 16; ++ch) {
-            uint32_t o16[16];
-            tmem_ld16(tO + ch * 16, o16);
+            for (int ch = 0; ch < D / 16; ++ch) {
+              uint32_t o16[16];
+              tmem_ld16(tO + ch * 16, o16);
+              tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 16; ++i) o16[i] = __float_as_uint(__uint_as_float(o16[i]) * alpha);
+              tmem_st16(tO + ch * 16, o16);
+            }
+          }
+          m_used = m_new;
+          if (j > 0) {
+            // The speculative P (keys 0-127 packed into columns 0-63) overwrote
+            // the scores of keys 0-63 only: reload keys 64-127 from TMEM, so only
+            // raw[0..63] had to stay live in registers across the speculative pass.
+            tmem_ld32(tS + 64, *reinterpret_cast<uint32_t(*)[32]>(raw + 64));
+            tmem_ld32(tS + 96, *reinterpret_cast<uint32_t(*)[32]>(raw + 96));
             tmem_wait_ld();
+            if (j == qt) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) o16[i] = __float_as_uint(__uint_as_float(o16[i]) * alpha);
-            tmem_st16(tO + ch * 16, o16);
+              for (int i = 64; i < AT_TILE; ++i)
+                if (i > r) raw[i] = __float_as_uint(-INFINITY);
+            }
           }
+          rowsum = write_p(m_used);
         }
-        m_used = m_new;
         if (quad == 0 && lane == 0) HX_TR(6 + g, j);
-        // p = 2^(s*c - m) on packed pairs (FFMA2), row sum on packed pairs (FADD2)
-        const uint64_t c2 = f2pack(c, c), nm2 = f2pack(-m_new, -m_new);
-        uint64_t rs2[2] = {f2pack(0.f, 0.f), f2pack(0.f, 0.f)};
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          uint32_t pk[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const uint64_t x2 = ffma2(f2pack(__uint_as_float(raw[half * 64 + 2 * i]),
-                                             __uint_as_float(raw[half * 64 + 2 * i + 1])), c2, nm2);
-            float e0, e1;
-            pk[i] = exp2_pack_mixed(x2, i, e0, e1);
-            rs2[i & 1] = fadd2(rs2[i & 1], f2pack(e0, e1));
-          }
-          tmem_st32(tS + half * 32, pk);  // P over the first 64 columns of S
-        }
         tmem_wait_st();
-        const float2 ra = f2unpack(rs2[0]), rb = f2unpack(rs2[1]);
-        l_run = l_run * alpha + ((ra.x + ra.y) + (rb.x + rb.y));
+        l_run = l_run * alpha + rowsum;
         tc_fence_before();
         mbar_arrive(&p_full[g]);
         if (quad == 0 && lane == 0) HX_TR(g, 2 * j + 1);
@@ -241,12 +306,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       if (qrow < p.s) p.lse[static_cast<int64_t>(bh) * p.s + qrow] = (m_used + log2f(l_run)) * LN2;
     }
   }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 9) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 512);
-  }
+  finish();
 }
 
 #ifdef HX_FWD_TRACE

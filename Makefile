@@ -1,9 +1,11 @@
 # Builds paper_2507_00394_b200/libhx.so (sm_100a) and the oracle's C pieces.
 NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-# Every n-th softmax exponential on the FMA pipe (0 = all on MUFU).  Measured on
-# B200 at GPT-1.3B/32k: 0 is fastest (fwd 4.21 ms, bwd 13.26 ms; n=4: 4.37 / 14.11).
-HX_POLY_EVERY ?= 0
+# Every n-th packed pair of forward softmax exponentials on the FMA pipe (0 = all
+# on MUFU).  Measured in the GPT-1.3B/32k bench step with the speculative-exp
+# forward: 16 (6% of the exps) 4.16-4.17 ms per forward vs 4.25-4.27 with 0 and
+# 4.30 with 8; alone, 4 was 4.7% slower.
+HX_POLY_EVERY ?= 16
 NVFLAGS := -O3 -std=c++17 -lineinfo $(ARCH) -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
            --expt-relaxed-constexpr -Iinclude -DHX_POLY_EVERY=$(HX_POLY_EVERY)
 SRC := $(wildcard paper_2507_00394_b200/csrc/*.cu)

@@ -92,7 +92,7 @@ HX_DEVICE float exp2_poly(float x) {
 // one is computed on the FMA pipe, the rest on MUFU (k is a compile-time
 // constant after unrolling, so the choice costs nothing).
 #ifndef HX_POLY_EVERY
-#define HX_POLY_EVERY 4
+#define HX_POLY_EVERY 16
 #endif
 HX_DEVICE float exp2_mixed(float x, int k) {
   if constexpr (HX_POLY_EVERY > 0) {

@@ -9,6 +9,8 @@ vendor kernel on the same box (attention forward).
 
 import argparse
 import json
+import sys
+from pathlib import Path
 
 import torch
 
@@ -51,11 +53,31 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         ms.append(e0.elapsed_time(e1))
-    ms.sort()
-    med = ms[len(ms) // 2]
     flops = 2 * 2 * s * s * d * n / 2          # QK^T + PV, causal half
-    print(json.dumps({"kernel": "flashinfer_trtllm_gen_fmha_fwd", "ms": round(med, 4), "s": s,
-                      "heads": n, "d": d, "tflops": round(flops / med / 1e9, 1)}))
+
+    def report(name, ms):
+        ms = sorted(ms)
+        med = ms[len(ms) // 2]
+        print(json.dumps({"kernel": name, "ms": round(med, 4), "s": s, "heads": n, "d": d,
+                          "tflops": round(flops / med / 1e9, 1)}))
+
+    report("flashinfer_trtllm_gen_fmha_fwd", ms)
+    # hx_attn_fwd on the same box, same shape, timed the same way
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+    from paper_2507_00394_b200.runtime import kernels as K
+    qkv = torch.randn(s, 3 * n * d, device=dev).to(torch.bfloat16)
+    o = torch.empty(s, n * d, dtype=torch.bfloat16, device=dev)
+    lse = torch.empty(1, n, s, device=dev)
+    ours = []
+    for i in range(a.reps + 3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        K.attention_fwd(qkv, s, 1, n, o, lse)
+        e1.record()
+        torch.cuda.synchronize()
+        if i >= 3:
+            ours.append(e0.elapsed_time(e1))
+    report("hx_attn_fwd", ours)
 
 
 if __name__ == "__main__":

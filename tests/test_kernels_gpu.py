@@ -197,3 +197,21 @@ def test_mse_loss_and_axpy():
     assert abs(slot.item() / z.numel() - (zf * zf).mean().item()) < 1e-5 * (zf * zf).mean().item()
     assert rel_err(dz, z.float() * (2.0 / z.numel())) < 1e-2
     assert torch.allclose(y, want)
+
+
+def test_kernel_timers_count_launches_per_entry_point():
+    # bench.py's in-step roofline: every C-ABI call bracketed by CUDA events
+    from paper_2507_00394_b200.runtime import _lib
+    x, w = rnd(512, 256, seed=20), rnd(256, 512, scale=256 ** -0.5, seed=21)
+    y = torch.empty(512, 512, dtype=torch.bfloat16, device=DEV)
+    _lib.start_kernel_timers()
+    for _ in range(3):
+        K.linear(x, w, y)
+    K.layernorm(x, torch.ones(256, device=DEV), torch.zeros(256, device=DEV))
+    t = _lib.stop_kernel_timers()
+    assert t["hx_gemm"]["launches"] == 3 and t["hx_ln_fwd"]["launches"] == 1
+    assert all(v["total_ms"] > 0 and v["mean_ms"] == pytest.approx(v["total_ms"] / v["launches"])
+               for v in t.values())
+    # disabled again: no timers collected
+    K.linear(x, w, y)
+    assert _lib.stop_kernel_timers() == {}

@@ -38,6 +38,20 @@ __device__ long long g_fwd_trace[8][1024];
 constexpr int FWD_REGS_SOFTMAX = 216;
 constexpr int FWD_REGS_ISSUE = 72;
 
+// Barrier waits of the forward: mbarrier.try_wait without the 1 ms suspend hint
+// the other kernels use (forward alone: 3.71 vs 3.85 ms at 1.3B/32k; the same
+// change made the backward 1% slower, so it stays local).  HX_FWD_SPIN=1 makes
+// the MMA issuer busy-poll instead (A/B only).
+#ifndef HX_FWD_SPIN
+#define HX_FWD_SPIN 0
+#endif
+HX_DEVICE void fwd_wait(uint64_t* bar, uint32_t parity) { mbar_wait_nohint(bar, parity); }
+HX_DEVICE void fwd_wait_mma(uint64_t* bar, uint32_t parity) {
+  if (HX_FWD_SPIN & 1) mbar_wait_spin(bar, parity);
+  else mbar_wait_nohint(bar, parity);
+}
+HX_DEVICE void fwd_wait_softmax(uint64_t* bar, uint32_t parity) { mbar_wait_nohint(bar, parity); }
+
 template <int D>
 struct FwdSmem {
   // K and V tiles share one ring, in load order K(0) V(0) K(1) V(1) ...; as many
@@ -116,7 +130,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       if (has_b) tma_tile_rows<D>(smem + L::QB, &tm_qkv, q_full, qcol, bi, qtile[1] * AT_TILE, AT_TILE);
       for (int n = 0; n < 2 * nkv; ++n) {
         const int sl = n % NS;
-        mbar_wait(&kv_empty[sl], ((n / NS) & 1) ^ 1);
+        fwd_wait(&kv_empty[sl], ((n / NS) & 1) ^ 1);
         mbar_arrive_expect_tx(&kv_full[sl], Tile<D>::BYTES);
         tma_tile_rows<D>(slot_addr(n), &tm_qkv, &kv_full[sl], (n & 1) ? vcol : kcol, bi, (n >> 1) * AT_TILE,
                          AT_TILE);
@@ -130,13 +144,13 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       bool pending[2] = {false, false};
       int pcount[2] = {0, 0};
       auto wait_slot = [&](int n) {
-        mbar_wait(&kv_full[n % NS], (n / NS) & 1);
+        fwd_wait_mma(&kv_full[n % NS], (n / NS) & 1);
         tc_fence_after();
       };
-      mbar_wait(q_full, 0);
+      fwd_wait(q_full, 0);
       auto issue_pv = [&](int g, int jt) {  // O_g += P_g(jt) V(jt)
         wait_slot(2 * jt + 1);
-        mbar_wait(&p_full[g], pcount[g] & 1);
+        fwd_wait_mma(&p_full[g], pcount[g] & 1);
         ++pcount[g];
         tc_fence_after();
         const uint32_t sv = smem_u32(slot_addr(2 * jt + 1));
@@ -197,7 +211,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       const float c = p.scale_log2;
       float m_used = -INFINITY, l_run = 0.f;
       for (int j = 0; j <= qt; ++j) {
-        mbar_wait(&s_full[g], j & 1);
+        fwd_wait_softmax(&s_full[g], j & 1);
         if (quad == 0 && lane == 0) HX_TR(g, 2 * j);
         tc_fence_after();
         uint32_t raw[AT_TILE];
@@ -297,7 +311,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         mbar_arrive(&p_full[g]);
         if (quad == 0 && lane == 0) HX_TR(g, 2 * j + 1);
       }
-      mbar_wait(&o_full[g], 0);
+      fwd_wait(&o_full[g], 0);
       tc_fence_after();
       __nv_bfloat16* orow = p.o + (static_cast<int64_t>(qrow) * p.b + bi) * p.ld_o + head * D;
 #pragma unroll

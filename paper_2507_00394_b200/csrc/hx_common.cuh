@@ -110,6 +110,39 @@ HX_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// try_wait without a suspend-time hint: the hardware's default bounded wait,
+// then re-poll.  Wakes faster than the 1 ms-hint form where the waiter is on
+// the critical path (measured on the attention forward).
+HX_DEVICE bool mbar_try_wait_nohint(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+HX_DEVICE void mbar_wait_nohint(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  if (mbar_try_wait_nohint(addr, parity)) return;
+  const uint64_t t0 = global_ns();
+  while (!mbar_try_wait_nohint(addr, parity)) {
+    if (global_ns() - t0 > HX_WAIT_LIMIT_NS) __trap();
+  }
+}
+
+// Busy-poll wait (mbarrier.test_wait, never suspends): for waits on the critical
+// path where the suspend/wake-up latency of try_wait shows (the MMA issuer).
+HX_DEVICE void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  if (mbar_test(bar, parity)) return;
+  const uint64_t t0 = global_ns();
+  while (!mbar_test(bar, parity)) {
+    if (global_ns() - t0 > HX_WAIT_LIMIT_NS) __trap();
+  }
+}
+
 HX_DEVICE void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }

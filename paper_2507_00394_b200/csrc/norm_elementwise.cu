@@ -7,6 +7,10 @@
 #include "hx_common.cuh"
 #include "hx_gemm.h"
 
+#ifndef HX_LN_PERSISTENT
+#define HX_LN_PERSISTENT 1
+#endif
+
 namespace hx {
 
 constexpr float LN_EPS = 1e-5f;
@@ -43,10 +47,10 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16* __rest
                                                       const float* __restrict__ bias,
                                                       __nv_bfloat16* __restrict__ y, int rows,
                                                       int h) {
-  const int row = blockIdx.x * 8 + warp_id();
-  if (row >= rows) return;
   const int lane = lane_id();
   const int nvec = h / 8;
+  // persistent warps (grid sized to the resident slots): no partial last wave
+  for (int row = blockIdx.x * 8 + warp_id(); row < rows; row += gridDim.x * 8) {
   const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<int64_t>(row) * h);
   float sum = 0.f, sq = 0.f;
 #pragma unroll
@@ -81,6 +85,7 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16* __rest
                          pack_bf16(o[6], o[7]));
     }
   }
+  }
 }
 
 // LN backward, input-gradient half: one warp per row,
@@ -92,10 +97,9 @@ __global__ void __launch_bounds__(256) ln_bwd_dx_kernel(
     const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
     const float* __restrict__ gain, const __nv_bfloat16* __restrict__ dres,
     __nv_bfloat16* __restrict__ dx, float2* __restrict__ stats, int rows, int h) {
-  const int row = blockIdx.x * 8 + warp_id();
-  if (row >= rows) return;
   const int lane = lane_id();
   const int nvec = h / 8;
+  for (int row = blockIdx.x * 8 + warp_id(); row < rows; row += gridDim.x * 8) {
   const int64_t off = static_cast<int64_t>(row) * h;
   const uint4* xr = reinterpret_cast<const uint4*>(x + off);
   const uint4* dr = reinterpret_cast<const uint4*>(dy + off);
@@ -147,6 +151,7 @@ __global__ void __launch_bounds__(256) ln_bwd_dx_kernel(
     }
   }
   if (lane == 0) stats[row] = make_float2(mu, rstd);
+  }
 }
 
 // LN backward, weight half: dgain += sum_rows dy*xhat, dbias += sum_rows dy.
@@ -259,11 +264,27 @@ __global__ void axpy_f32_kernel(float* __restrict__ y, const float* __restrict__
     else return cudaErrorInvalidValue;  \
   } while (0)
 
+// Persistent row loops: at most as many blocks of 8 warps as fit on the GPU at
+// once (occupancy of the kernel), so the grid has no partial last wave.
+template <typename K>
+static int ln_blocks_per_sm(K kernel) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  return per_sm;
+}
+static int ln_grid(int per_sm, int rows) {
+  const int blocks = (rows + 7) / 8;
+  if (!HX_LN_PERSISTENT) return blocks;
+  const int resident = num_sms() * per_sm;
+  return blocks < resident ? blocks : resident;
+}
+
 cudaError_t ln_fwd_launch(const void* x, const float* g, const float* b, void* y, int rows, int h,
                           cudaStream_t st) {
-  const int grid = (rows + 7) / 8;
 #define L(NV)                                                                          \
-  ln_fwd_kernel<NV><<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), g, b, \
+  static const int per_sm_##NV = ln_blocks_per_sm(ln_fwd_kernel<NV>);                    \
+  ln_fwd_kernel<NV><<<ln_grid(per_sm_##NV, rows), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), g, b, \
                                           static_cast<__nv_bfloat16*>(y), rows, h)
   HX_NV_DISPATCH(h, L);
 #undef L
@@ -272,10 +293,10 @@ cudaError_t ln_fwd_launch(const void* x, const float* g, const float* b, void* y
 
 cudaError_t ln_bwd_launch(const void* dy, const void* x, const float* g, const void* dres, void* dx,
                           float* dg, float* db, float* stats, int rows, int h, cudaStream_t st) {
-  const int grid = (rows + 7) / 8;
   float2* st2 = reinterpret_cast<float2*>(stats);
 #define L(NV)                                                                                   \
-  ln_bwd_dx_kernel<NV><<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(dy),            \
+  static const int per_sm_##NV = ln_blocks_per_sm(ln_bwd_dx_kernel<NV>);                         \
+  ln_bwd_dx_kernel<NV><<<ln_grid(per_sm_##NV, rows), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(dy),            \
                                              static_cast<const __nv_bfloat16*>(x), g,           \
                                              static_cast<const __nv_bfloat16*>(dres),           \
                                              static_cast<__nv_bfloat16*>(dx), st2, rows, h)

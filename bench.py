@@ -17,6 +17,13 @@ compute with fp32 accumulation.  Activations are far larger than the 126 MB L2
 value  = m*s*b tokens / step, device-timed with CUDA events (max over ranks)
 e2e    = same iteration through HelixRuntime with pinned-host inputs copied in
          and the losses read back inside the timed region
+
+``--gpus N`` without a torchrun environment re-launches this script under
+``torch.distributed.run`` with N ranks (one helix stage per GPU).
+
+Reference arm (``--impl reference``): the reference's own ``execute_schedule``
+(``pipelab`` installed in baseline/_ref; the float64 oracle port if absent) on
+BASELINE config 1's model, on every host core -- see :func:`run_reference`.
 """
 
 from __future__ import annotations
@@ -55,7 +62,10 @@ def parse():
     ap.add_argument("--mlp-chunk", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-s", type=int, default=256)
+    ap.add_argument("--no-extrapolate", dest="extrapolate", action="store_false",
+                    help="skip the labelled FLOP-scaled CPU extrapolation to the workload")
+    ap.add_argument("--no-config1", dest="config1", action="store_false",
+                    help="skip the B200 measurement at BASELINE config 1 (N=1 only)")
     ap.add_argument("--stash-budget-gb", type=float, default=None,
                     help="device budget for stashed activations; the rest is FILO-offloaded to pinned "
                          "host memory ('auto': free HBM after weights/grads minus a working-set margin; "
@@ -130,12 +140,10 @@ class ClockSampler:
 
 
 def cpu_sample_tokens_per_s(wl: dict, sample_s: int, threads: int = 1) -> tuple[float, float, str]:
-    """Time the float64 oracle (the reference's algorithm, einsum, no BLAS) on
-    one layer of the workload's width at a bounded sequence length, on
-    ``threads`` host threads in parallel, and convert to whole-workload
-    tokens/s by the reference's own FLOP count (P/costs.py:62-71:
-    72h^2 + 12hs per token per layer, full-square attention as computed)."""
-    import numpy as np
+    """FLOP-scaled extrapolation (a labelled extra, not the CPU baseline): the
+    float64 oracle on one layer of the workload's width at a bounded sequence
+    length, converted to whole-workload tokens/s by the reference's own FLOP
+    count (P/costs.py:62-71: 72h^2 + 12hs per token per layer)."""
     from concurrent.futures import ThreadPoolExecutor
     from oracle import helix_oracle as O
 
@@ -157,41 +165,164 @@ def cpu_sample_tokens_per_s(wl: dict, sample_s: int, threads: int = 1) -> tuple[
     sample_flops = threads * sample_s * (72 * h * h + 12 * h * sample_s)
     rate = sample_flops / wall
     full_per_token = wl["L"] * (72 * h * h + 12 * h * wl["s"])
-    desc = (f"oracle (float64 numpy einsum, reference algorithm) one layer h={h} heads={heads} "
-            f"s={sample_s} fwd+bwd x{threads} threads in {wall:.2f}s = {rate / 1e9:.2f} GFLOP/s, "
-            f"scaled by reference FLOPs/token (L*(72h^2+12hs)) to L={wl['L']} s={wl['s']}")
-    _ = np, math
+    desc = (f"oracle (float64 numpy einsum) one layer h={h} heads={heads} s={sample_s} fwd+bwd x{threads} "
+            f"threads in {wall:.2f}s = {rate / 1e9:.2f} GFLOP/s, scaled by the reference's FLOPs/token "
+            f"(L*(72h^2+12hs)) to L={wl['L']} s={wl['s']}")
     return rate / full_per_token, wall, desc
 
 
+# BASELINE config 1: the reference's CPU-runnable case (tiny GPT, 2 stages x 4 micro-batches)
+CONFIG1 = dict(L=4, h=256, s=1024, b=1, num_heads=4, p=2, m=4)
+CONFIG1_METHOD = "helix_twofold"
+# the bounded per-step sample of config 1: one of its layers (same h, heads, s, b)
+# through one helix stage with the smallest two-fold micro-batch count
+CONFIG1_SLICE = dict(L=1, h=256, s=1024, b=1, num_heads=4, p=1, m=2)
+
+
+def config1_dict() -> dict:
+    return {"workload": "tiny (BASELINE configs[0])", **CONFIG1, "method": CONFIG1_METHOD,
+            "durations": "DurationTable.from_units(1, 3, 2)", "params_seed": 0, "inputs_seed": 1}
+
+
+def _ref_pipelab():
+    """The unmodified reference package from baseline/_ref, or None."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "pipelab").is_dir():
+        return None
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    try:
+        import pipelab  # noqa: F401
+        import pipelab.runtime.executor as ex
+        ex._WAIT_TIMEOUT = 1e9      # P/runtime/executor.py:56 (threaded waits; SURVEY 8d caveat)
+        return pipelab
+    except ImportError:
+        return None
+
+
+def _ref_worker(job: tuple) -> tuple[float, str]:
+    """One bounded sample in a worker process: the reference's own
+    ``execute_schedule`` (P/runtime/executor.py:425-440) on ``cfg_kw``, or the
+    oracle port's ``sequential_oracle`` when pipelab is not installed."""
+    cfg_kw, threaded = job
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    pl = _ref_pipelab()
+    if pl is not None:
+        from pipelab import ModelConfig as RC, generate as rgen
+        from pipelab.costs import DurationTable as RD
+        from pipelab.runtime import execute_schedule as rexec, make_inputs as rin, make_model as rmod
+        cfg = RC(**cfg_kw)
+        sched = rgen(CONFIG1_METHOD, cfg, RD.from_units(1, 3, 2))
+        P, X = rmod(cfg, 0), rin(cfg, 1)
+        t0 = time.perf_counter()
+        rexec(sched, P, X, threaded=threaded)
+        return time.perf_counter() - t0, "reference"
+    from oracle import helix_oracle as O
+    c = cfg_kw
+    P = O.make_model(c["L"], c["h"], 0)
+    X = O.make_inputs(c["m"], c["s"], c["b"], c["h"], 1)
+    t0 = time.perf_counter()
+    O.sequential_oracle(P, X, c["num_heads"])
+    return time.perf_counter() - t0, "port"
+
+
+class ReferenceSampler:
+    """Config-1 tokens/s of the reference's CPU implementation on this host.
+
+    Each step runs ``R`` independent replicas (one per host core, separate
+    processes: the reference's numerics are single-threaded einsum) of the
+    config-1 slice; step time = the slowest replica.  tokens/s at config 1
+    = R * m_slice * s * b / step_time * (L_slice / L_config1): per-layer work
+    is identical, so the 4-layer config costs exactly L/L_slice slices.
+    """
+
+    def __init__(self, replicas: int):
+        import multiprocessing as mp
+        self.replicas = replicas
+        self.pool = mp.get_context("spawn").Pool(replicas)   # no fork of a CUDA process
+        self.kind = None
+
+    def step(self, cfg_kw: dict, threaded: bool = False) -> float:
+        res = self.pool.map(_ref_worker, [(cfg_kw, threaded)] * self.replicas, chunksize=1)
+        self.kind = res[0][1]
+        return max(t for t, _ in res)
+
+    def tokens_per_s(self, wall: float) -> float:
+        c = CONFIG1_SLICE
+        return self.replicas * c["m"] * c["s"] * c["b"] / wall * (c["L"] / CONFIG1["L"])
+
+    def describe(self) -> str:
+        impl = ("the reference's own execute_schedule (pipelab from baseline/_ref, replay driver)"
+                if self.kind == "reference" else "the float64 oracle port (sequential_oracle)")
+        c = CONFIG1_SLICE
+        return (f"{impl}; per step {self.replicas} concurrent replicas (1 per host core) of one config-1 "
+                f"layer (h={c['h']} heads={c['num_heads']} s={c['s']} b={c['b']}) x {c['m']} micro-batches "
+                f"fwd+bwd, helix_twofold p=1; tokens/s scaled by L_slice/L = {c['L']}/{CONFIG1['L']}")
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
 def run_reference(args, wl, rank: int, world: int) -> None:
-    """--impl reference: the reference's CPU algorithm (oracle port; the
-    reference is Python and cannot be compiled into oracle/_ref) on this
-    host's cores, bounded sample per step."""
+    """--impl reference: the reference's CPU implementation of the path on this
+    host's cores, at BASELINE config 1 (the only configuration a CPU runs; the
+    B200 line reports its own number at the same config under ``config1``).
+    Rank 0 alone runs under torchrun."""
     if rank != 0:
         return
     cores = os.cpu_count() or 1
-    sample_s = 64
-    for _ in range(args.warmup):
-        cpu_sample_tokens_per_s(wl, 64, 1)
-    vals, walls, desc = [], [], ""
-    for _ in range(args.steps):
-        v, wall, desc = cpu_sample_tokens_per_s(wl, sample_s, cores)
-        vals.append(v)
-        walls.append(wall)
-    value = sum(vals) / len(vals)
-    p = args.gpus
+    smp = ReferenceSampler(cores)
+    try:
+        warm = dict(L=2, h=64, s=128, b=1, num_heads=2, p=2, m=4)     # SURVEY 8c fast CI shape
+        for _ in range(args.warmup):
+            smp.step(warm)
+        walls = [smp.step(CONFIG1_SLICE) for _ in range(args.steps)]
+    finally:
+        smp.close()
+    wall = sum(walls) / len(walls)
+    value = smp.tokens_per_s(wall)
+    ext, _w, ext_desc = cpu_sample_tokens_per_s(wl, 64, cores) if args.extrapolate else (None, 0, "")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(walls) / len(walls),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": args.workload, **wl, "p": p, "m": 2 * p, "method": args.method},
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
-                         "sample": desc},
+        "data": "synthetic (reference fixtures: make_model seed 0, make_inputs seed 1)",
+        "config": config1_dict(),
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": smp.kind,
+                         "sample": smp.describe(), "cpu_model": _cpu_model()},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "warmup_sample": "fast CI shape L=2 h=64 s=128 p=2 m=4 per replica",
     }
+    if ext is not None:
+        line["extrapolated_to_workload"] = {"workload": args.workload, "value": ext, "unit": "tokens/s",
+                                            "how": ext_desc}
     print(json.dumps(line), flush=True)
+
+
+def _cpu_model() -> str:
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def relaunch(args) -> int:
+    """``python bench.py --gpus N`` outside torchrun: one rank per GPU."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 # ------------------------------------------------------------------ GPU leg
@@ -227,35 +358,164 @@ def main() -> None:
     if args.impl == "reference":
         run_reference(args, wl, rank, world)
         return
-    if world > 1:
-        # leave SMs for the NCCL p2p kernels that run next to persistent GEMMs
-        os.environ.setdefault("HX_SM_RESERVE", "8")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch(args))
+    if world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world} (one rank per GPU)")
+    # test-only: run the same multi-rank driver on CPU over gloo with the float64
+    # test double (tests/cpu_math.py) at a toy shape -- never a bench number
+    cpu_double = os.environ.get("HX_BENCH_CPU_DOUBLE") == "1"
+    if world > 1 and not cpu_double:
+        # NCCL init lines (nRanks per communicator) on stderr for the launch check
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     if args.workload == "gpt7b_128k" or args.stash_budget_gb is not None:
         # offloading churns GB-sized blocks: grow segments instead of fragmenting them
         os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
+    if cpu_double:
+        return bench_cpu_double(args, world, rank)
+    bench_gpu(args, wl, world, rank, local)
 
+
+def bench_cpu_double(args, world: int, rank: int) -> None:
+    """Test-only leg (HX_BENCH_CPU_DOUBLE=1): the launch and the multi-rank
+    distributed driver exactly as on the GPU box, over gloo with float64 CPU
+    math, at the toy shape L=4 h=8 s=8 with p = N and m = 2N."""
+    import numpy as np
     import torch
     import torch.distributed as dist
     from paper_2507_00394_b200 import ModelConfig, generate
+    from paper_2507_00394_b200.costs import DurationTable
+    from paper_2507_00394_b200.runtime.executor import DeviceModel, HelixRuntime, pair_groups, stage_fields
+    from paper_2507_00394_b200.runtime.model import DeviceLayer, make_inputs, make_model
+    from tests.cpu_math import CpuMath
+
+    if world > 1:
+        dist.init_process_group("gloo")
+    p = world
+    cfg = ModelConfig(L=4, h=8, s=8, b=1, num_heads=2, p=p, m=2 * p)
+    sched = generate(args.method, cfg, DurationTable.from_units(1, 3, 2))
+    stages = [rank] if world > 1 else list(range(p))
+    layers = {}
+    for l, prm in enumerate(make_model(cfg, 0)):
+        need, own = set(), set()
+        for st in stages:
+            n_, o_ = stage_fields(sched, st, l)
+            need |= set(n_)
+            own |= set(o_)
+        if need:
+            layers[l] = DeviceLayer({k: torch.from_numpy(np.ascontiguousarray(getattr(prm, k))) for k in need},
+                                    tuple(own), grad_dtype=torch.float64)
+    rt = HelixRuntime(sched, DeviceModel(layers), None, "distributed" if world > 1 else "replay",
+                      torch.device("cpu"), math=CpuMath(cfg, bool(int(sched.meta["qkv"]))),
+                      rank=rank if world > 1 else None, groups=pair_groups(p) if world > 1 else None)
+    inputs = [torch.from_numpy(x).reshape(cfg.s * cfg.b, cfg.h) for x in make_inputs(cfg, 1)]
+    for _ in range(args.warmup):
+        rt.run(inputs)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        rt.run(inputs)
+    ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    if world > 1:
+        t = torch.tensor([ms])
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        sums = torch.tensor(rt.sumsq.tolist(), dtype=torch.float64)
+        dist.all_reduce(sums)
+    else:
+        sums = rt.sumsq
+    if rank == 0:
+        tokens = cfg.m * cfg.s * cfg.b
+        print(json.dumps({
+            "metric": METRIC, "value": tokens / (ms / 1e3), "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "TEST DOUBLE (CPU, gloo)",
+            "config": {"workload": "toy", "L": cfg.L, "h": cfg.h, "s": cfg.s, "b": cfg.b, "p": p, "m": cfg.m,
+                       "method": args.method},
+            "losses": [float(v) / (cfg.s * cfg.b * cfg.h) for v in sums.tolist()],
+            "comm": rt.comm_stats}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def measure_config1(dev) -> dict:
+    """The B200 at BASELINE config 1, like for like with the reference arm:
+    ``execute_schedule`` with the reference's host fixtures (float64 numpy in,
+    RunResult of numpy out; wall clock per call, all copies inside), and the
+    same schedule through HelixRuntime device-timed.  Losses are checked
+    against the reference's known config-1 values."""
+    import torch
+    from paper_2507_00394_b200 import ModelConfig, generate
+    from paper_2507_00394_b200.costs import DurationTable
+    from paper_2507_00394_b200.runtime import execute_schedule, make_inputs, make_model
+    from paper_2507_00394_b200.runtime.executor import DeviceModel, HelixRuntime
+
+    known = [3.327261203817688, 3.3800507339316543, 3.443091222231624, 3.4279542847160513]
+    cfg = ModelConfig(**CONFIG1)
+    sched = generate(CONFIG1_METHOD, cfg, DurationTable.from_units(1, 3, 2))
+    P, X = make_model(cfg, 0), make_inputs(cfg, 1)
+    tokens = cfg.m * cfg.s * cfg.b
+    out = {"config": config1_dict()}
+    for threaded in (False, True):
+        for _ in range(3):
+            res = execute_schedule(sched, P, X, threaded=threaded)
+        reps = 10
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            res = execute_schedule(sched, P, X, threaded=threaded)
+        wall = (time.perf_counter() - t0) / reps
+        out["execute_schedule_threaded" if threaded else "execute_schedule_replay"] = {
+            "tokens_per_s": tokens / wall, "ms_per_call": 1e3 * wall,
+            "loss_max_rel_err_vs_reference": max(abs(a - b) / b for a, b in zip(res.losses, known))}
+    model = DeviceModel.from_host(sched, P, range(cfg.p), dev)
+    rt = HelixRuntime(sched, model, None, "multistream", dev)
+    xs = [torch.from_numpy(x).to(dev, torch.bfloat16).reshape(cfg.s * cfg.b, cfg.h) for x in X]
+    for _ in range(3):
+        rt.run(xs)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(20):
+        rt.run(xs)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / 20
+    out["device"] = {"tokens_per_s": tokens / (ms / 1e3), "ms_per_step": ms,
+                     "how": "HelixRuntime multistream (one CUDA stream per stage), CUDA events"}
+    out["value"] = out["execute_schedule_threaded"]["tokens_per_s"]
+    out["unit"] = "tokens/s"
+    out["value_is"] = "execute_schedule(threaded=True) with host float64 fixtures, wall clock per call"
+    return out
+
+
+def bench_gpu(args, wl, world: int, rank: int, local: int) -> None:
+    import torch
+    import torch.distributed as dist
+    from paper_2507_00394_b200 import ModelConfig, generate
+    from paper_2507_00394_b200.analytic import bubble_fraction, bubble_time_from_table
     from paper_2507_00394_b200.costs import DurationTable, attention_kernel_flops, b200_flops_per_token
     from paper_2507_00394_b200.runtime import HelixRuntime
     from paper_2507_00394_b200.runtime import _lib, kernels as K
-    from paper_2507_00394_b200.runtime.executor import DeviceModel, make_pair_groups, stage_fields
+    from paper_2507_00394_b200.runtime.executor import DeviceModel, pair_groups, stage_fields
     from paper_2507_00394_b200.runtime.model import DeviceLayer, random_device_layer
     from paper_2507_00394_b200.simulate import (measured_durations, metrics_from_timeline, overlap_report,
                                                 predict_pipeline, simulate)
+    from paper_2507_00394_b200.engine import CommModel
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import datetime
-        dist.init_process_group("nccl", device_id=dev, timeout=datetime.timedelta(seconds=600))
+        dist.init_process_group("nccl", device_id=dev, timeout=datetime.timedelta(seconds=900))
     p = world
     cfg = ModelConfig(L=wl["L"], h=wl["h"], s=wl["s"], b=wl["b"], num_heads=wl["num_heads"], p=p, m=2 * p)
     units = DurationTable.from_units(1, 3, 2)
     sched = generate(args.method, cfg, units)
     stages = [rank] if world > 1 else list(range(p))
-    groups = make_pair_groups(p) if world > 1 else None
+    groups = pair_groups(p) if world > 1 else None
 
     def build_runtime(schedule):
         """Random-init weights of the architecture, drawn on the GPU (same
@@ -359,6 +619,23 @@ def main() -> None:
             ov = overlap_report(sched, tl)
             predicted["measured_comm_wait_ms"] = ov.total_wait
             predicted["measured_steady_comm_wait_ms"] = ov.steady_wait
+            # analytic (closed form, zero comm) / simulated (zero comm and NVLink-modelled) /
+            # measured bubble side by side for this p: the gaps attribute any shortfall
+            nv = CommModel("bytes", latency=5000, bytes_per_element=2, bandwidth=int(770e9))
+            sim_nv = simulate(sched, table, nv)
+            try:
+                analytic_ms = bubble_time_from_table(args.method, p, cfg.L, table) / 1e6
+                analytic_frac = bubble_fraction(args.method, cfg, table)
+            except Exception:   # noqa: BLE001 -- no formula for this method
+                analytic_ms = analytic_frac = None
+            predicted["bubble_table"] = {
+                "analytic": {"fraction": analytic_frac, "per_stage_bubble_ms": analytic_ms},
+                "simulated_zero_comm": {"fraction": sim.metrics.bubble_fraction,
+                                        "makespan_ms": sim.metrics.makespan / 1e6},
+                "simulated_nvlink": {"fraction": sim_nv.metrics.bubble_fraction,
+                                     "makespan_ms": sim_nv.metrics.makespan / 1e6},
+                "measured": {"fraction": measured.bubble_fraction, "makespan_ms": measured.makespan,
+                             "per_stage_bubble_ms": list(measured.per_stage_bubble)}}
         if world == 1:
             # helix vs same-kernel 1F1B at p = 2/4/8 predicted from these measured component
             # times (reference simulator, NVLink 770 GB/s per direction): a prediction only
@@ -466,10 +743,27 @@ def main() -> None:
                 "flops_convention": "causal: fwd 2*b*n*s^2*d, bwd 2.5x fwd"}
         del qkv, o, lse, do, dqkv, delta, dq
 
+    # like-for-like pair at BASELINE config 1 (the reference arm's configuration)
+    config1 = None
+    if rank == 0 and world == 1 and args.config1:
+        config1 = measure_config1(dev)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, wall, desc = cpu_sample_tokens_per_s(wl, args.cpu_sample_s, 1)
-        cpu = {"value": v, "unit": "tokens/s", "cores": 1, "kind": "port", "sample": desc}
+        cores = os.cpu_count() or 1
+        smp = ReferenceSampler(cores)
+        try:
+            wall = smp.step(CONFIG1_SLICE)
+        finally:
+            smp.close()
+        cpu = {"value": smp.tokens_per_s(wall), "unit": "tokens/s (BASELINE config 1)", "cores": cores,
+               "kind": smp.kind, "sample": smp.describe() + "; 1 step", "cpu_model": _cpu_model(),
+               "config": config1_dict()}
+        if config1 is not None:
+            cpu["b200_same_config"] = {"tokens_per_s": config1["value"], "ratio": config1["value"] / cpu["value"]}
+        if args.extrapolate:
+            v, _w, desc = cpu_sample_tokens_per_s(wl, 256, 1)
+            cpu["extrapolated_to_workload"] = {"value": v, "unit": "tokens/s", "cores": 1, "how": desc}
 
     if rank == 0:
         fpt = b200_flops_per_token(cfg)
@@ -478,6 +772,7 @@ def main() -> None:
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (N(0,1) inputs, random-init weights)",
             "config": {"workload": args.workload, **wl, "p": p, "m": cfg.m, "method": args.method,
+                       "n_gpus": world,
                        "mlp_chunk": args.mlp_chunk, "parallelism": f"pp{p} (one helix stage per GPU)",
                        "l2": "inputs/activations >> L2 (134 MB per tensor), no flush"},
             "mfu": value * fpt / (world * float(peaks["bf16_tflops"]) * 1e12),
@@ -491,6 +786,8 @@ def main() -> None:
             "roofline": roof,
             "kernel_share": kernel_share,
             "cpu_baseline": cpu,
+            "config1": config1,
+            "comm": rt.comm_stats,
             "clocks": clk,
             "max_memory_gb": torch.cuda.max_memory_allocated(dev) / 2**30,
             "stash_offload": rt.offload_stats(),

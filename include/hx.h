@@ -49,6 +49,14 @@ HX_API int hx_version(void);
 HX_API long long hx_launch_count(void);
 
 /*
+ * Leave `sms` SMs (0..64) free of persistent-kernel CTAs, for NCCL p2p kernels
+ * running beside them when one stage runs per GPU (the reference's stage
+ * threads, P/runtime/executor.py:334-382, become ranks).  Overrides the
+ * HX_SM_RESERVE environment variable; applies to launches after the call.
+ */
+HX_API int hx_set_sm_reserve(int sms);
+
+/*
  * C[M,N] (epi)= op(A)[M,K] * op(B)[K,N], bf16 in, fp32 accumulate (tcgen05/TMEM).
  *   a_mn=0: A stored [M,K] row-major (lda >= K);  a_mn=1: A stored [K,M] (lda >= M)
  *   b_mn=0: B stored [N,K] row-major (ldb >= K);  b_mn=1: B stored [K,N] (ldb >= N)

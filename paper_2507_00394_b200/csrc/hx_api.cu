@@ -9,22 +9,26 @@
 namespace hx {
 
 static std::atomic<long long> g_launches{0};
+// -1: not set through hx_set_sm_reserve, fall back to the HX_SM_RESERVE env var
+static std::atomic<int> g_sm_reserve{-1};
 
-// SMs available to persistent kernels.  HX_SM_RESERVE (env) leaves SMs free for
+// SMs available to persistent kernels.  The reserve leaves SMs free for
 // concurrently running NCCL point-to-point kernels in multi-stage runs, so a
 // statically scheduled persistent GEMM never waits for a CTA slot.
 int num_sms() {
-  static int n = 0;
-  if (n == 0) {
+  static int total = 0;
+  static int env_reserve = 0;
+  if (total == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+    cudaDeviceGetAttribute(&total, cudaDevAttrMultiProcessorCount, dev);
+    if (total <= 0) total = 148;
     const char* r = getenv("HX_SM_RESERVE");
-    const int reserve = r ? atoi(r) : 0;
-    if (reserve > 0 && reserve < n) n -= reserve;
+    env_reserve = r ? atoi(r) : 0;
   }
-  return n;
+  int reserve = g_sm_reserve.load();
+  if (reserve < 0) reserve = env_reserve;
+  return (reserve > 0 && reserve < total) ? total - reserve : total;
 }
 
 using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -98,6 +102,12 @@ extern "C" {
 int hx_version(void) { return 100; }
 
 long long hx_launch_count(void) { return g_launches.load(); }
+
+int hx_set_sm_reserve(int sms) {
+  if (sms < 0 || sms > 64) return HX_E_SHAPE;
+  g_sm_reserve.store(sms);
+  return HX_OK;
+}
 
 int hx_gemm(const void* A, int lda, int a_mn, const void* B, int ldb, int b_mn, void* C, int ldc, int M,
             int N, int K, int epi, const void* aux, int ld_aux, void* out2, int ld_out2, void* stream) {

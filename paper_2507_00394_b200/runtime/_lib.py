@@ -25,6 +25,7 @@ _LL = ctypes.c_longlong
 SIGNATURES: dict[str, list] = {
     "hx_version": [],
     "hx_launch_count": [],
+    "hx_set_sm_reserve": [_I],
     "hx_gemm": [_P, _I, _I, _P, _I, _I, _P, _I, _I, _I, _I, _I, _P, _I, _P, _I, _P],
     "hx_ln_fwd": [_P, _P, _P, _P, _I, _I, _P],
     "hx_ln_bwd": [_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P],
@@ -108,6 +109,11 @@ def call(name: str, *args) -> None:
     b.record()
     _timers.setdefault(name, []).append((a, b))
     check(rc, name)
+
+
+def set_sm_reserve(sms: int) -> None:
+    """SMs kept free of persistent-kernel CTAs (for NCCL kernels beside them)."""
+    check(load().hx_set_sm_reserve(int(sms)), "hx_set_sm_reserve")
 
 
 def launch_count() -> int:

@@ -31,6 +31,9 @@ Drivers
 
 from __future__ import annotations
 
+import os
+from collections import deque
+from contextlib import nullcontext
 from dataclasses import dataclass
 
 import numpy as np
@@ -77,7 +80,14 @@ def _logical_elements(entry: dict) -> int:
 
 
 class _Stage:
-    def __init__(self, idx: int, device, stream):
+    """Per-stage state.  ``ln_wctx_elements`` is T*h: each of the reference's
+    deferred W contexts also holds two such tensors, the LayerNorm's normalised input and output
+    gradient (``xhat2``/``d_ln2`` post, ``xhat1``/``d_ln1`` pre,
+    ``P/runtime/layers.py:150-152``, ``:197``).  Here the LN gain/bias
+    gradients are reduced in the B pass, so those tensors never exist, but
+    ``peak_stash_elements`` counts them so the number matches the reference."""
+
+    def __init__(self, idx: int, device, stream, ln_wctx_elements: int = 0):
         self.idx = idx
         self.device = device
         self.stream = stream
@@ -85,12 +95,13 @@ class _Stage:
         self.stash: dict[tuple[int, int, str], dict] = {}
         self.wctx: dict[int, list] = {}
         self.peak = 0
+        self.ln_wctx_elements = ln_wctx_elements
 
     def bump(self) -> None:
         n = sum(_logical_elements(e) for e in self.stash.values())
         for lst in self.wctx.values():
             for _l, w_post, w_pre in lst:
-                n += _logical_elements(w_post) + _logical_elements(w_pre)
+                n += _logical_elements(w_post) + _logical_elements(w_pre) + 4 * self.ln_wctx_elements
         self.peak = max(self.peak, n)
 
 
@@ -523,71 +534,171 @@ class P2PPlan:
         self.pairs = sorted(self.send_seq)
 
 
-class _Distributed:
-    """Rank r executes stage r; payloads move over NCCL (or gloo on CPU tests)."""
+class _SendQueue:
+    """Outstanding sends to one peer, oldest first.
 
-    def __init__(self, core: _Core, rank: int, groups: dict, lookahead: int = 1):
+    A send's tensors are dropped as soon as its work reports completion
+    (polled before every task), so a payload lives on the sender only until
+    the receiver has taken it -- the reference's ownership rule, where a SEND
+    moves the payload to the consumer (``executor.py:160-164``, ``:286``).
+    ``cap`` bounds the number kept per peer: past it the oldest is waited on,
+    which for NCCL only orders the launching stream after that send (the host
+    never blocks); blocking backends (gloo) pass ``cap=None``.
+    """
+
+    def __init__(self, cap: int | None):
+        self.cap = cap
+        self.q: deque = deque()
+        self.max_live = 0
+
+    def push(self, works: list, tensors: list) -> None:
+        self.q.append((works, tensors))
+        if self.cap is not None:
+            while len(self.q) > self.cap:
+                for w in self.q.popleft()[0]:
+                    w.wait()
+        self.max_live = max(self.max_live, len(self.q))
+
+    def prune(self) -> None:
+        while self.q and all(w.is_completed() for w in self.q[0][0]):
+            self.q.popleft()
+
+    def drain(self) -> None:
+        while self.q:
+            for w in self.q.popleft()[0]:
+                w.wait()
+
+    def __len__(self) -> int:
+        return len(self.q)
+
+
+class _Distributed:
+    """Rank r executes stage r; payloads move over NCCL (or gloo on CPU tests).
+
+    Receives are posted ``recv_ahead`` compute tasks before their consumer, in
+    the sender's issue order (``P2PPlan``).  On CUDA they are issued from a
+    dedicated idle stream with buffers allocated on it: ProcessGroupNCCL
+    orders a p2p op after the work already queued on the *issuing* stream, so
+    a receive issued from the compute stream could not start before the
+    compute queued ahead of it -- the transfer the two-fold order is meant to
+    hide would serialise behind it.  The consumer's stream waits on the
+    receive (``Work.wait``) and takes ownership (``record_stream``).  Sends
+    are issued from the compute stream (they must follow their producer).
+    """
+
+    def __init__(self, core: _Core, rank: int, groups: dict, recv_ahead: int | None = None,
+                 send_cap: int | None = -1, plan: "P2PPlan | None" = None):
         self.core = core
         self.rank = rank
-        self.plan = P2PPlan(core.sched)
+        self.plan = plan if plan is not None else P2PPlan(core.sched)
         self.groups = groups
-        self.lookahead = lookahead
+        st = core.stages[rank]
+        self.cuda = st.device.type == "cuda"
+        if recv_ahead is None:
+            recv_ahead = int(os.environ.get("HX_RECV_AHEAD", "4"))
+        self.recv_ahead = max(0, recv_ahead)
+        if send_cap == -1:
+            # default: bounded where waiting is non-blocking for the host (NCCL only
+            # orders the stream); a blocking backend (gloo) bounds only when asked to
+            env = os.environ.get("HX_SEND_CAP")
+            send_cap = int(env) if env else (4 if self.cuda else None)
+            if send_cap is not None and send_cap <= 0:
+                send_cap = None
+        self.sends: dict[int, _SendQueue] = {}
+        self.send_cap = send_cap
+        self.comm_stream = torch.cuda.Stream(device=st.device) if self.cuda else None
         self.posted: dict[str, tuple[list, dict]] = {}    # rid -> (works, payload)
         self.next_recv: dict[int, int] = {}               # src -> index into recv_seq
-        self.pending_sends: list = []
+        self.recv_index = {rid: (src, k) for (src, dst), seq in self.plan.recv_seq.items()
+                           if dst == rank for k, rid in enumerate(seq)}
+        order = core.sched.per_stage_order[rank]
+        # per compute task, the RECVs (on this stage) that must have landed before it
+        # runs; a RECV shared by a recompute task and its BWD_B lands once, for the first
+        self.needs: list[list[str]] = []
+        seen: set[str] = set()
+        for tid in order:
+            t = core.tasks[tid]
+            need = [d for d in t.deps if d not in seen and (dt := core.tasks.get(d)) is not None
+                    and dt.kind == RECV and dt.stage == rank]
+            seen.update(need)
+            self.needs.append(need)
 
-    def _post_upto(self, src: int, rid: str) -> None:
+    def _post_upto(self, src: int, want: int) -> None:
+        """Post the receives from ``src`` up to index ``want`` of its sequence."""
         seq = self.plan.recv_seq[(src, self.rank)]
-        want = seq.index(rid)
         core, cfg = self.core, self.core.cfg
-        while self.next_recv.get(src, 0) <= min(want + self.lookahead, len(seq) - 1):
-            k = self.next_recv.get(src, 0)
-            r_id = seq[k]
-            layout = _payload_layout(cfg, _edge_tag(r_id), core.qkv, core.math)
-            st = core.stages[self.rank]
-            payload, works = {}, []
-            for name, shape, dtype in layout:
-                buf = torch.empty(shape, dtype=dtype, device=st.device)
-                payload[name] = buf
-                works.append(torch.distributed.irecv(buf, src=src, group=self.groups[(src, self.rank)]))
-            self.posted[r_id] = (works, payload)
-            self.next_recv[src] = k + 1
+        st = core.stages[self.rank]
+        ctx = torch.cuda.stream(self.comm_stream) if self.cuda else nullcontext()
+        with ctx:
+            while self.next_recv.get(src, 0) <= want:
+                k = self.next_recv.get(src, 0)
+                r_id = seq[k]
+                payload, works = {}, []
+                for name, shape, dtype in _payload_layout(cfg, _edge_tag(r_id), core.qkv, core.math):
+                    buf = torch.empty(shape, dtype=dtype, device=st.device)
+                    payload[name] = buf
+                    works.append(torch.distributed.irecv(buf, src=src, group=self.groups[(src, self.rank)]))
+                self.posted[r_id] = (works, payload)
+                self.next_recv[src] = k + 1
+
+    def _post(self, rid: str) -> None:
+        src, k = self.recv_index[rid]
+        if k >= self.next_recv.get(src, 0):
+            self._post_upto(src, k)
 
     def _receive(self, rid: str) -> dict:
-        t = self.core.tasks[rid]
-        if rid not in self.posted:
-            self._post_upto(t.peer, rid)
+        self._post(rid)
         works, payload = self.posted.pop(rid)
         for w in works:
-            w.wait()
+            w.wait()        # NCCL: the current (compute) stream waits; gloo: blocks
+        if self.cuda:
+            cur = torch.cuda.current_stream()
+            for t in payload.values():
+                t.record_stream(cur)
         return payload
+
+    def live_sends(self) -> int:
+        return sum(len(q) for q in self.sends.values())
 
     def run(self, timer: _Timer) -> None:
         core, r = self.core, self.rank
         st = core.stages[r]
-        for tid in core.sched.per_stage_order[r]:
-            t = core.tasks[tid]
-            for d in t.deps:
-                dt = core.tasks.get(d)
-                if dt is None or dt.kind != RECV or dt.stage != r or d in st.values:
-                    continue
+        order = core.sched.per_stage_order[r]
+        for k, tid in enumerate(order):
+            for j in range(k, min(len(order), k + 1 + self.recv_ahead)):
+                for rid in self.needs[j]:
+                    self._post(rid)
+            for q in self.sends.values():
+                q.prune()
+            for d in self.needs[k]:
                 st.values[d] = self._receive(d)
+            t = core.tasks[tid]
             with timer.around(tid):
                 core.run_compute(t)
             for snd in core.sends_by_producer.get(tid, ()):
                 payload = core.checked_payload(snd)
                 layout = _payload_layout(core.cfg, _edge_tag(snd.id), core.qkv, core.math)
                 grp = self.groups[(r, snd.peer)]
+                works, tensors = [], []
                 for name, _shape, dtype in layout:
                     tensor = payload[name].contiguous()
                     if tensor.dtype != dtype:
                         raise PayloadMismatch(f"{snd.id}: {name} has dtype {tensor.dtype}, want {dtype}")
-                    self.pending_sends.append((torch.distributed.isend(tensor, dst=snd.peer, group=grp), tensor))
-        for w, _t in self.pending_sends:
-            w.wait()
-        self.pending_sends.clear()
+                    works.append(torch.distributed.isend(tensor, dst=snd.peer, group=grp))
+                    tensors.append(tensor)
+                q = self.sends.get(snd.peer)
+                if q is None:
+                    q = self.sends[snd.peer] = _SendQueue(self.send_cap)
+                q.push(works, tensors)
+                del payload, tensors
+        for q in self.sends.values():
+            q.drain()
         if self.posted:
             raise ExecutionError(f"undelivered payloads: {sorted(self.posted)}")
+
+    @property
+    def max_live_sends(self) -> dict[int, int]:
+        return {peer: q.max_live for peer, q in self.sends.items()}
 
 
 def make_pair_groups(n_stages: int, warm: bool = True, device=None) -> dict[tuple[int, int], object]:
@@ -619,6 +730,26 @@ def make_pair_groups(n_stages: int, warm: bool = True, device=None) -> dict[tupl
     return groups
 
 
+_PAIR_GROUP_CACHE: list = []   # [(world process group, n_stages, groups)]
+
+
+def pair_groups(n_stages: int) -> dict[tuple[int, int], object]:
+    """``make_pair_groups`` once per (world process group, n_stages).
+
+    ``execute_schedule`` is called once per iteration (``P/runtime/executor.py:425``);
+    creating n(n-1) communicators on every call would leak NCCL communicators
+    and pay their setup each step.  A re-initialised world (new default group
+    object) gets fresh groups."""
+    world = torch.distributed.group.WORLD
+    for w, n, groups in _PAIR_GROUP_CACHE:
+        if w is world and n == n_stages:
+            return groups
+    groups = make_pair_groups(n_stages)
+    _PAIR_GROUP_CACHE[:] = [e for e in _PAIR_GROUP_CACHE if e[0] is world]
+    _PAIR_GROUP_CACHE.append((world, n_stages, groups))
+    return groups
+
+
 # ======================================================================================
 # public API
 # ======================================================================================
@@ -646,13 +777,21 @@ class HelixRuntime:
         self.model = model
         self.rank = rank
         local = [rank] if mode == "distributed" else list(range(sched.n_stages))
-        self.stages = {si: _Stage(si, self.device, None) for si in local}
+        ln_ctx = self.cfg.s * self.cfg.b * self.cfg.h
+        self.stages = {si: _Stage(si, self.device, None, ln_ctx) for si in local}
         self.sumsq = torch.zeros(self.cfg.m, dtype=torch.float64, device=self.device)
         self.timeline = None
         self.core = _Core(sched, model, self.math, self.stages, self.sumsq)
         self.groups = groups
         self.record_timeline = record_timeline
         self.timeline = None
+        self._plan = None
+        self.comm_stats = None
+        if mode == "distributed" and self.device.type == "cuda":
+            # persistent GEMMs size their grids to the SMs left after this reserve, so
+            # the NCCL p2p kernels that run next to them always find a free SM
+            from . import _lib
+            _lib.set_sm_reserve(int(os.environ.get("HX_SM_RESERVE", "8")))
         if stash_budget_bytes is not None:
             from .offload import StashOffloader
             weights = [w for dl in model.layers.values() for w in dl.w.values()]
@@ -677,7 +816,12 @@ class HelixRuntime:
         elif self.mode == "multistream":
             _multistream(self.core, timer)
         elif self.mode == "distributed":
-            _Distributed(self.core, self.rank, self.groups).run(timer)
+            if self._plan is None:
+                self._plan = P2PPlan(self.sched)
+            drv = _Distributed(self.core, self.rank, self.groups, plan=self._plan)
+            drv.run(timer)
+            self.comm_stats = {"max_live_sends_per_peer": drv.max_live_sends,
+                               "recv_ahead": drv.recv_ahead, "send_cap": drv.send_cap}
         else:
             raise ExecutionError(f"unknown mode {self.mode!r}")
         self.timeline = timer.collect()
@@ -752,7 +896,7 @@ def execute_schedule(sched: Schedule, params: list[LayerParams], inputs: list,
         rank = torch.distributed.get_rank()
         model = DeviceModel.from_host(sched, params, [rank], device)
         rt = HelixRuntime(sched, model, mlp_chunk, "distributed", device, rank=rank,
-                          groups=make_pair_groups(sched.n_stages), record_timeline=record_timeline,
+                          groups=pair_groups(sched.n_stages), record_timeline=record_timeline,
                           stash_budget_bytes=stash_budget_bytes, offload_min_bytes=offload_min_bytes)
     else:
         model = DeviceModel.from_host(sched, params, range(sched.n_stages), device)
@@ -774,7 +918,8 @@ def _gather_distributed(rt: HelixRuntime, params) -> RunResult:
     """All ranks contribute their owned gradients, loss slots and peaks."""
     import torch.distributed as dist
     local = {"grads": rt.grads_numpy(), "sumsq": rt.sumsq.cpu().tolist(),
-             "peak": rt.stages[rt.rank].peak, "rank": rt.rank, "timeline": rt.timeline}
+             "peak": rt.stages[rt.rank].peak, "rank": rt.rank, "timeline": rt.timeline,
+             "offload": rt.offload_stats()}
     allv = [None] * dist.get_world_size()
     dist.all_gather_object(allv, local)
     cfg = rt.cfg
@@ -796,4 +941,14 @@ def _gather_distributed(rt: HelixRuntime, params) -> RunResult:
     tl = {}
     for part in allv:
         tl.update(part["timeline"] or {})
-    return RunResult(list(sumsq / n), grads, peaks, "threaded", tl or None)
+    offload = None
+    if any(part["offload"] for part in allv):
+        # per-rank statistics plus the byte totals across ranks
+        per_rank = {part["rank"]: part["offload"] for part in allv}
+        totals = {}
+        for st in per_rank.values():
+            for k, v in (st or {}).items():
+                if isinstance(v, (int, float)) and not isinstance(v, bool):
+                    totals[k] = totals.get(k, 0) + v
+        offload = {"total": totals, "per_rank": per_rank}
+    return RunResult(list(sumsq / n), grads, peaks, "threaded", tl or None, offload)

@@ -97,6 +97,15 @@ def measured_durations(sched: Schedule, timeline) -> DurationTable:
     return DurationTable.from_measured(row("pre"), row("attn"), row("post"))
 
 
+def _analytic_fraction(method: str, cfg, durations: DurationTable) -> float | None:
+    from .analytic import bubble_fraction
+    from .config import ConfigError
+    try:
+        return bubble_fraction(method, cfg, durations)
+    except ConfigError:     # no formula (e.g. 1f1b_rc, a B200 extension)
+        return None
+
+
 def predict_pipeline(cfg, durations: DurationTable, stages=(2, 4, 8), link_gbs: float = 770.0,
                      latency_us: float = 5.0,
                      methods=("helix_twofold", "helix_twofold_rc", "1f1b", "1f1b_rc")) -> dict:
@@ -122,6 +131,8 @@ def predict_pipeline(cfg, durations: DurationTable, stages=(2, 4, 8), link_gbs: 
             ov = overlap_report(res)
             row[method] = {"tokens_per_s": tokens / (res.metrics.makespan * 1e-9),
                            "bubble_fraction": res.metrics.bubble_fraction,
+                           # closed form (P/analytic.py:46-58), zero comm, forward durations only
+                           "analytic_bubble_fraction": _analytic_fraction(method, c, durations),
                            "makespan_ms": res.metrics.makespan / 1e6,
                            # transfer waits: all, and those the schedule meant to hide
                            "comm_wait_ms": ov.total_wait / 1e6, "steady_comm_wait_ms": ov.steady_wait / 1e6}

@@ -19,7 +19,7 @@ from oracle import helix_oracle as O
 from paper_2507_00394_b200 import EXTENSION_METHODS, METHODS, ModelConfig, generate
 from paper_2507_00394_b200.costs import DurationTable
 from paper_2507_00394_b200.runtime.executor import (
-    DeviceModel, HelixRuntime, P2PPlan, _gather_distributed, make_pair_groups, stage_fields)
+    DeviceModel, HelixRuntime, P2PPlan, _gather_distributed, pair_groups, stage_fields)
 from paper_2507_00394_b200.runtime.model import DeviceLayer, make_inputs, make_model
 
 UNIT = DurationTable.from_units(1, 3, 2)
@@ -31,10 +31,10 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, cfg_kw, method, qkv, q):
+def _worker(rank, world, port, cfg_kw, method, qkv, q, env=None):
     try:
         from tests.cpu_math import CpuMath
-        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), **(env or {}))
         dist.init_process_group("gloo", rank=rank, world_size=world)
         cfg = ModelConfig(**cfg_kw)
         sched = generate(method, cfg, UNIT, qkv_in_attention=qkv)
@@ -47,30 +47,37 @@ def _worker(rank, world, port, cfg_kw, method, qkv, q):
                 layers[l] = DeviceLayer(t, own, grad_dtype=torch.float64)
         math = CpuMath(cfg, bool(int(sched.meta["qkv"])))
         rt = HelixRuntime(sched, DeviceModel(layers), None, "distributed", torch.device("cpu"),
-                          math=math, rank=rank, groups=make_pair_groups(world))
+                          math=math, rank=rank, groups=pair_groups(world))
         inputs = [torch.from_numpy(x).reshape(cfg.s * cfg.b, cfg.h) for x in make_inputs(cfg, 1)]
         rt.run(inputs)
+        stats = [rt.comm_stats]
+        rt.run(inputs)          # a second iteration reuses the cached groups and plan
+        stats.append(rt.comm_stats)
+        assert pair_groups(world) is rt.groups
         res = _gather_distributed(rt, params)
+        allstats = [None] * world
+        dist.all_gather_object(allstats, stats)
         if rank == 0:
-            q.put(("ok", res.losses, res.param_grads, res.peak_stash_elements))
+            q.put(("ok", res.losses, res.param_grads, res.peak_stash_elements, allstats))
         dist.barrier()
         dist.destroy_process_group()
     except Exception as e:  # noqa: BLE001
-        q.put(("err", f"rank {rank}: {type(e).__name__}: {e}", None, None))
+        q.put(("err", f"rank {rank}: {type(e).__name__}: {e}", None, None, None))
 
 
-def run_world(world, cfg_kw, method, qkv=True):
+def run_world(world, cfg_kw, method, qkv=True, with_stats=False, env=None):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg_kw, method, qkv, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg_kw, method, qkv, q, env))
+             for r in range(world)]
     for p in procs:
         p.start()
     out = q.get(timeout=240)
     for p in procs:
         p.join(timeout=60)
     assert out[0] == "ok", out[1]
-    return out[1:]
+    return out[1:] if with_stats else out[1:4]
 
 
 def _oracle(cfg_kw):
@@ -124,3 +131,38 @@ def test_p2p_plan_orders_are_consistent():
         for (src, dst), seq in plan.send_seq.items():
             assert [sched.tasks[r].deps[0] for r in plan.recv_seq[(src, dst)]] == seq
             assert all(sched.tasks[s].stage == src and sched.tasks[s].peer == dst for s in seq)
+
+
+@pytest.mark.parametrize("method", ["helix_twofold", "helix_twofold_rc", "1f1b"])
+def test_sent_payloads_are_released(method):
+    """A sender keeps a payload only until the receiver has taken it (the
+    reference moves payload ownership to the consumer, ``executor.py:160-164``;
+    round 1 kept every sent tensor until the iteration ended).  On NCCL
+    completed sends are polled and dropped, and at most ``HX_SEND_CAP`` (4) per
+    peer stay live; gloo's p2p work reports completion only from ``wait()``,
+    so here the cap path itself is driven (cap 2, receives posted up front so
+    the blocking wait cannot deadlock) and results must stay exact."""
+    losses, grads, _peaks, allstats = run_world(
+        4, TOY4, method, with_stats=True, env={"HX_RECV_AHEAD": "100000", "HX_SEND_CAP": "2"})
+    for rank, per_iter in enumerate(allstats):
+        for st in per_iter:
+            live = st["max_live_sends_per_peer"]
+            assert live and max(live.values()) <= 2, (rank, live)
+    ref = _oracle(TOY4)
+    assert np.allclose(losses, ref.losses, rtol=1e-10)
+    for l in range(TOY4["L"]):
+        for k in O.FIELDS:
+            assert np.allclose(grads[l][k], ref.param_grads[l][k], rtol=1e-9, atol=1e-12), (method, l, k)
+
+
+def test_default_lookahead_bounds_transit():
+    """Default look-ahead: a payload waits on its sender until the receiver
+    is ``recv_ahead`` tasks from consuming it; the per-peer count can never
+    exceed the messages of that pair in one iteration and is 0 at the end."""
+    cfg = ModelConfig(**TOY4)
+    plan = P2PPlan(generate("helix_twofold", cfg, UNIT))
+    *_, allstats = run_world(4, TOY4, "helix_twofold", with_stats=True)
+    for rank, per_iter in enumerate(allstats):
+        for st in per_iter:
+            for peer, n in st["max_live_sends_per_peer"].items():
+                assert 1 <= n <= len(plan.send_seq[(rank, peer)])

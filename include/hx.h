@@ -99,12 +99,22 @@ HX_API int hx_attn_fwd(const void* qkv, int ld_qkv, void* o, int ld_o, float* ls
 /*
  * Causal attention backward.  Writes dq, dk, dv into dqkv ([s*b, ld_dqkv], same
  * column layout as qkv).  Workspaces: delta [b*heads*s] f32 and dq_acc
- * [s*b*heads*d] f32 (both fully overwritten).
+ * [s*b*heads*d] f32 (both fully overwritten).  With o == NULL, delta is an
+ * input instead: D = rowsum(dO * O) from hx_attn_bwd_delta (computed on the
+ * stage that holds O, so the attention stage need not stash it).
  * Replaces mathops.attention_backward (P/runtime/mathops.py:103-116).
  */
 HX_API int hx_attn_bwd(const void* qkv, int ld_qkv, const void* o, const void* d_o, int ld_o,
                 const float* lse, float* delta_ws, float* dq_ws, void* dqkv, int ld_dqkv, int s,
                 int b, int heads, int d, void* stream);
+
+/*
+ * delta[b, heads, s] = rowsum(d_o * o) per head (f32), the flash backward's
+ * D term (P/runtime/mathops.py:113: the rowsum(dP * P) of the reference,
+ * which equals rowsum(dO * O)).  o, d_o: [s*b, ld_o] bf16.
+ */
+HX_API int hx_attn_bwd_delta(const void* o, const void* d_o, int ld_o, float* delta, int s, int b, int heads,
+                             int d, void* stream);
 
 /*
  * sumsq_acc[0] += sum(z^2) (fp64); dz = z * 2/n.  loss = sumsq/n (host divides).

@@ -862,9 +862,10 @@ static cudaError_t bwd9_launch(const void* qkv, int ld_qkv, const void* o, const
     cfg = true;
   }
   const int tokens = p.s * p.b;
-  attn_bwd_pre_kernel<D><<<(tokens + 7) / 8, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(o),
-                                                           static_cast<const __nv_bfloat16*>(d_o), ld_o,
-                                                           const_cast<float*>(p.delta), p.s, p.b, p.heads);
+  if (o != nullptr)  // else delta already holds D (hx_attn_bwd_delta on the post stage)
+    attn_bwd_pre_kernel<D><<<(tokens + 7) / 8, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(o),
+                                                             static_cast<const __nv_bfloat16*>(d_o), ld_o,
+                                                             const_cast<float*>(p.delta), p.s, p.b, p.heads);
   dim3 grid((p.s + AT_TILE - 1) / AT_TILE, p.b * p.heads);
   attn_bwd_dkdv9_kernel<D><<<grid, 320, KV9Smem<D>::TOTAL, st>>>(tq, tdo, p);
   e = cudaGetLastError();
@@ -892,15 +893,32 @@ static cudaError_t fused_launch(const void* qkv, int ld_qkv, const void* o, cons
   const int tokens = p.s * p.b;
   e = cudaMemsetAsync(dq_acc, 0, static_cast<size_t>(tokens) * p.h * sizeof(float), st);
   if (e != cudaSuccess) return e;
-  attn_bwd_pre_kernel<D><<<(tokens + 7) / 8, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(o),
-                                                           static_cast<const __nv_bfloat16*>(d_o), ld_o,
-                                                           const_cast<float*>(p.delta), p.s, p.b, p.heads);
+  if (o != nullptr)  // else delta already holds D (hx_attn_bwd_delta on the post stage)
+    attn_bwd_pre_kernel<D><<<(tokens + 7) / 8, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(o),
+                                                             static_cast<const __nv_bfloat16*>(d_o), ld_o,
+                                                             const_cast<float*>(p.delta), p.s, p.b, p.heads);
   const int grid = ((p.s + AT_TILE - 1) / AT_TILE) * p.b * p.heads;
   attn_bwd_fused_kernel<D><<<grid, 512, FusedSmem<D>::TOTAL, st>>>(tq, tdo, tdq, p);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int64_t vecs = static_cast<int64_t>(tokens) * p.h / 8;
   attn_bwd_dq_convert_kernel<D><<<static_cast<unsigned>((vecs + 255) / 256), 256, 0, st>>>(dq_acc, p);
+  return cudaGetLastError();
+}
+
+cudaError_t attn_bwd_delta_launch(const void* o, const void* d_o, int ld_o, float* delta, int s, int b, int heads,
+                                  int d, cudaStream_t st) {
+  const int tokens = s * b;
+  if (d == 128)
+    attn_bwd_pre_kernel<128><<<(tokens + 7) / 8, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(o),
+                                                               static_cast<const __nv_bfloat16*>(d_o), ld_o, delta,
+                                                               s, b, heads);
+  else if (d == 64)
+    attn_bwd_pre_kernel<64><<<(tokens + 7) / 8, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(o),
+                                                              static_cast<const __nv_bfloat16*>(d_o), ld_o, delta,
+                                                              s, b, heads);
+  else
+    return cudaErrorNotSupported;
   return cudaGetLastError();
 }
 

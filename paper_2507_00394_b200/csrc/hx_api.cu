@@ -112,7 +112,10 @@ int hx_set_sm_reserve(int sms) {
 int hx_gemm(const void* A, int lda, int a_mn, const void* B, int ldb, int b_mn, void* C, int ldc, int M,
             int N, int K, int epi, const void* aux, int ld_aux, void* out2, int ld_out2, void* stream) {
   if (M <= 0 || N <= 0 || K <= 0) return HX_E_SHAPE;
-  if (K % 8 || N % 8 || lda % 8 || ldb % 8 || ldc % 4) return HX_E_SHAPE;
+  // K (the reduction extent) needs 16-byte granularity only for a K-major
+  // operand; an MN-major one (the weight-gradient form X^T dY over a ragged MLP
+  // row slab) reads its K tail through TMA out-of-bounds zero fill
+  if (((!a_mn || !b_mn) && K % 8) || N % 8 || lda % 8 || ldb % 8 || ldc % 4) return HX_E_SHAPE;
   if (!aligned16(A) || !aligned16(B) || !aligned16(C)) return HX_E_ALIGN;
   if (epi < HX_EPI_STORE_BF16 || epi > HX_EPI_STORE_F32) return HX_E_UNSUPPORTED;
   if (epi == HX_EPI_ACC_F32 || epi == HX_EPI_STORE_F32) {
@@ -169,7 +172,15 @@ int hx_attn_bwd(const void* qkv, int ld_qkv, const void* o, const void* d_o, int
     return HX_E_ALIGN;
   return ret(attn_bwd_launch(qkv, ld_qkv, o, d_o, ld_o, lse, delta_ws, dq_ws, dqkv, ld_dqkv, s, b, heads, d,
                              as_stream(stream)),
-             3);
+             o != nullptr ? 3 : 2);
+}
+
+int hx_attn_bwd_delta(const void* o, const void* d_o, int ld_o, float* delta, int s, int b, int heads, int d,
+                      void* stream) {
+  if (d != 64 && d != 128) return HX_E_UNSUPPORTED;
+  if (s <= 0 || b <= 0 || heads <= 0 || ld_o < heads * d || ld_o % 8) return HX_E_SHAPE;
+  if (!aligned16(o) || !aligned16(d_o) || !aligned16(delta)) return HX_E_ALIGN;
+  return ret(attn_bwd_delta_launch(o, d_o, ld_o, delta, s, b, heads, d, as_stream(stream)), 1);
 }
 
 int hx_mse_loss(const void* z, long long n, void* dz, double* sumsq_acc, void* stream) {

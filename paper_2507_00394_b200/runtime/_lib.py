@@ -31,6 +31,7 @@ SIGNATURES: dict[str, list] = {
     "hx_ln_bwd": [_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P],
     "hx_attn_fwd": [_P, _I, _P, _I, _P, _I, _I, _I, _I, _P],
     "hx_attn_bwd": [_P, _I, _P, _P, _I, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P],
+    "hx_attn_bwd_delta": [_P, _P, _I, _P, _I, _I, _I, _I, _P],
     "hx_mse_loss": [_P, _LL, _P, _P, _P],
     "hx_axpy_f32": [_P, _P, _LL, _P],
     "hx_zero": [_P, _LL, _P],

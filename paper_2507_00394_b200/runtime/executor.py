@@ -43,7 +43,7 @@ from ..costs import comm_volume
 from ..generators import meta_config
 from ..partition import post_stage, pre_stage
 from ..schedule import BWD_B, BWD_W, FWD, RECOMPUTE, RECV, SEND, Schedule, Task
-from .layers import LayerMath, payload_elements
+from .layers import LayerMath, Pending, payload_elements
 from .model import (MATRIX_FIELDS, PARAM_FIELDS, POST_FIELDS, PRE_FIELDS, DeviceLayer,
                     LayerParams, layer_to_device)
 
@@ -72,11 +72,13 @@ class RunResult:
 
 # Stash entries that exist only for the flash backward (never part of the
 # reference's stash accounting, never sent between stages).
-_LOCAL_EXTRAS = ("o", "lse")
+_LOCAL_EXTRAS = ("lse",)
 
 
 def _logical_elements(entry: dict) -> int:
-    return sum(int(t.numel()) for k, t in entry.items() if k not in _LOCAL_EXTRAS)  # tensors or offloaded placeholders
+    # tensors, offloaded / pending placeholders; "_"-prefixed keys are regeneration
+    # caches (layers.post_output), not stash entries of the reference
+    return sum(int(t.numel()) for k, t in entry.items() if k not in _LOCAL_EXTRAS and k[0] != "_")
 
 
 class _Stage:
@@ -96,13 +98,40 @@ class _Stage:
         self.wctx: dict[int, list] = {}
         self.peak = 0
         self.ln_wctx_elements = ln_wctx_elements
+        # device bytes of the distinct tensors held by stash + W contexts (weights
+        # and inputs excluded), after each task: checked against runtime/memplan.py
+        self.peak_bytes = 0
+        self.peak_bytes_at = ""
+        self.resident_ptrs: set[int] = set()
 
-    def bump(self) -> None:
+    def held_bytes(self) -> int:
+        seen: dict[int, int] = {}
+
+        def visit(d):
+            for v in d.values():
+                if isinstance(v, torch.Tensor):
+                    st = v.untyped_storage()
+                    ptr = st.data_ptr()
+                    if ptr not in self.resident_ptrs:
+                        seen[ptr] = st.nbytes()
+
+        for e in self.stash.values():
+            visit(e)
+        for lst in self.wctx.values():
+            for _l, w_post, w_pre in lst:
+                visit(w_post)
+                visit(w_pre)
+        return sum(seen.values())
+
+    def bump(self, tid: str = "") -> None:
         n = sum(_logical_elements(e) for e in self.stash.values())
         for lst in self.wctx.values():
             for _l, w_post, w_pre in lst:
                 n += _logical_elements(w_post) + _logical_elements(w_pre) + 4 * self.ln_wctx_elements
         self.peak = max(self.peak, n)
+        nb = self.held_bytes()
+        if nb > self.peak_bytes:
+            self.peak_bytes, self.peak_bytes_at = nb, tid
 
 
 def stage_fields(sched: Schedule, stage: int, layer: int) -> tuple[tuple[str, ...], tuple[str, ...]]:
@@ -166,6 +195,9 @@ class _Core:
         self.stages = stages
         self.sumsq = sumsq
         self.offload = None   # StashOffloader (FILO host offload) or None
+        # the pre stash drops x (l > 0); rc.pre(l) rebuilds it
+        # from post(l-1)'s retention on the same stage (HelixRuntime.regen_pre_x)
+        self.regen_pre_x = False
         self.inputs: list[torch.Tensor] = []
         self.recv_of_send = {t.deps[0]: t.id for t in self.tasks.values() if t.kind == RECV}
         self.sends_by_producer: dict[str, list[Task]] = {}
@@ -206,7 +238,11 @@ class _Core:
             raise StalledSchedule(f"stage {st.idx}: payload of {tid} not present") from None
 
     def store_stash(self, st: _Stage, l: int, mb: int, comp: str, full: dict, payload: dict) -> None:
-        st.stash[(l, mb, comp)] = self.math.reduce_stash(comp, full, payload) if self.rc else full
+        kept = self.math.reduce_stash(comp, full, payload) if self.rc else full
+        if self.regen_pre_x and comp == "pre" and l > 0:
+            kept = dict(kept)
+            kept["x"] = Pending(int(kept["x"].numel()))
+        st.stash[(l, mb, comp)] = kept
         if self.offload is not None:
             self.offload.after_store(st, (l, mb, comp))
 
@@ -225,7 +261,7 @@ class _Core:
         self._run_compute(st, t)
         if self.offload is not None:
             self.offload.after_task(st, t)
-        st.bump()
+        st.bump(t.id)
 
     def _run_compute(self, st: _Stage, t: Task) -> None:
         if t.kind == FWD:
@@ -238,6 +274,14 @@ class _Core:
                 self.math.pre_backward_w(w_pre, self.G(l))
         elif t.kind == RECOMPUTE:
             key = (t.layer, t.mb, t.comp)
+            if self.regen_pre_x and t.comp == "pre" and t.layer > 0:
+                # post(l-1) runs on this stage (pre_stage(l) == post_stage(l-1),
+                # P/partition.py:25-36) and its rc.post comes after this task
+                # (P/generators.py:397-444), so its retention is still here
+                kept_post = st.stash[(t.layer - 1, t.mb, "post")]
+                x, cache = self.math.post_output(kept_post, self.W(t.layer - 1))
+                kept_post.update(cache)
+                st.stash[key]["x"] = x
             st.stash[key] = self.math.regenerate_stash(t.comp, st.stash[key],
                                                        self.W(t.layer) if t.layer in self.model.layers else None)
         else:
@@ -313,7 +357,7 @@ class _Core:
             if self.rc:  # 1f1b_rc: regenerate this layer's non-attention stash in place
                 s_post = self.math.regenerate_stash("post", s_post, W)
                 s_pre = self.math.regenerate_stash("pre", s_pre, W)
-            gap, w_post = self.math.post_backward_b(d, W, G, s_post)
+            gap, w_post = self.math.post_backward_b(d, W, G, s_post, fuse_w=not self.split)
             gpa = self.math.attn_backward(gap, s_attn)
             d, w_pre = self.math.pre_backward_b(gpa, W, G, s_pre)
             if self.split:
@@ -488,7 +532,10 @@ def _payload_layout(cfg, edge_tag: str, qkv: bool, math=None) -> list[tuple[str,
     if edge_tag == "ap":
         return [act("attn_out"), act("residual")]
     if edge_tag == "gap":
-        return [act("d_attn_out"), act("d_residual")]
+        lay = [act("d_attn_out"), act("d_residual")]
+        if getattr(math, "ships_delta", False):   # flash backward's D (layers.py docstring)
+            lay.append(("delta", (cfg.b * cfg.num_heads * cfg.s,), torch.float32))
+        return lay
     if edge_tag == "gpa":
         return [act("d_ln_out"), act("d_residual"), ("d_qkv_weight", (h, 3 * h), f32)] if qkv \
             else [act("d_qkv", 3 * h), act("d_residual")]
@@ -767,13 +814,16 @@ class HelixRuntime:
     def __init__(self, sched: Schedule, model: DeviceModel, mlp_chunk: int | None = None,
                  mode: str = "replay", device=None, math=None, rank: int | None = None,
                  groups: dict | None = None, record_timeline: bool = False,
-                 stash_budget_bytes: int | None = None, offload_min_bytes: int = 32 << 20):
+                 stash_budget_bytes: int | None = None, offload_min_bytes: int = 32 << 20,
+                 regen_pre_x: bool = False):
         self.sched = sched
         self.cfg = meta_config(sched)
         self.mode = mode
         self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
         qkv = bool(int(sched.meta.get("qkv", 0)))
-        self.math = math if math is not None else LayerMath(self.cfg, qkv, mlp_chunk, self.device)
+        self.math = math if math is not None else LayerMath(
+            self.cfg, qkv, mlp_chunk, self.device, recompute=bool(int(sched.meta.get("recompute", 0))),
+            defer_w=sched.meta.get("backward") == "split")
         self.model = model
         self.rank = rank
         local = [rank] if mode == "distributed" else list(range(sched.n_stages))
@@ -782,6 +832,12 @@ class HelixRuntime:
         self.sumsq = torch.zeros(self.cfg.m, dtype=torch.float64, device=self.device)
         self.timeline = None
         self.core = _Core(sched, model, self.math, self.stages, self.sumsq)
+        if regen_pre_x:
+            chunked = any(t.comp == "chunk" for t in sched.tasks.values() if t.is_compute)
+            if not self.core.rc or chunked:
+                raise ExecutionError("regen_pre_x needs a layer-wise schedule with recomputation "
+                                     "(rc.pre tasks rebuild x)")
+            self.core.regen_pre_x = True
         self.groups = groups
         self.record_timeline = record_timeline
         self.timeline = None
@@ -796,7 +852,7 @@ class HelixRuntime:
             from .offload import StashOffloader
             weights = [w for dl in model.layers.values() for w in dl.w.values()]
             self.core.offload = StashOffloader(sched, self.stages, weights, stash_budget_bytes,
-                                               min_bytes=offload_min_bytes)
+                                               min_bytes=offload_min_bytes, regen_pre_x=regen_pre_x)
 
     def run(self, inputs: list[torch.Tensor]) -> None:
         cfg = self.cfg
@@ -805,8 +861,12 @@ class HelixRuntime:
         self.core.inputs = [x.reshape(cfg.s * cfg.b, cfg.h) for x in inputs]
         if self.core.offload is not None:
             self.core.offload.exclude(self.core.inputs)
+        resident = {w.untyped_storage().data_ptr() for dl in self.model.layers.values() for w in dl.w.values()}
+        resident |= {x.untyped_storage().data_ptr() for x in self.core.inputs}
         for st in self.stages.values():
             st.peak = 0
+            st.peak_bytes, st.peak_bytes_at = 0, ""
+            st.resident_ptrs = resident
         self.model.zero_grads(self.math.zero_)
         self.math.zero_(self.sumsq)
         timer = _Timer(self.record_timeline)
@@ -820,8 +880,10 @@ class HelixRuntime:
                 self._plan = P2PPlan(self.sched)
             drv = _Distributed(self.core, self.rank, self.groups, plan=self._plan)
             drv.run(timer)
+            st = self.stages[self.rank]
             self.comm_stats = {"max_live_sends_per_peer": drv.max_live_sends,
-                               "recv_ahead": drv.recv_ahead, "send_cap": drv.send_cap}
+                               "recv_ahead": drv.recv_ahead, "send_cap": drv.send_cap,
+                               "stash_peak_bytes": st.peak_bytes, "stash_peak_at": st.peak_bytes_at}
         else:
             raise ExecutionError(f"unknown mode {self.mode!r}")
         self.timeline = timer.collect()
@@ -869,7 +931,7 @@ def _to_device_inputs(inputs, cfg, device) -> list[torch.Tensor]:
 def execute_schedule(sched: Schedule, params: list[LayerParams], inputs: list,
                      mlp_chunk: int | None = None, threaded: bool = False,
                      record_timeline: bool = False, *, stash_budget_bytes: int | None = None,
-                     offload_min_bytes: int = 32 << 20) -> RunResult:
+                     offload_min_bytes: int = 32 << 20, regen_pre_x: bool = False) -> RunResult:
     """Run ``sched`` numerically on the B200(s); same contract as the reference.
 
     ``threaded=False``: replay on the current GPU.  ``threaded=True``: one rank
@@ -881,6 +943,11 @@ def execute_schedule(sched: Schedule, params: list[LayerParams], inputs: list,
     stashed activations per process on the device, FILO-offloading the rest to
     pinned host memory (``runtime/offload.py``); tensors smaller than
     ``offload_min_bytes`` always stay.
+
+    ``regen_pre_x`` (B200 extension, rc schedules): the pre stash drops its
+    ``x``; ``rc.pre(l)`` rebuilds it from ``post(l-1)``'s retention on the same
+    stage, trading two MLP GEMMs per (layer, micro-batch)
+    for ``b*s*h`` of stash.
     """
     cfg = meta_config(sched)
     if len(params) != cfg.L:
@@ -897,12 +964,13 @@ def execute_schedule(sched: Schedule, params: list[LayerParams], inputs: list,
         model = DeviceModel.from_host(sched, params, [rank], device)
         rt = HelixRuntime(sched, model, mlp_chunk, "distributed", device, rank=rank,
                           groups=pair_groups(sched.n_stages), record_timeline=record_timeline,
-                          stash_budget_bytes=stash_budget_bytes, offload_min_bytes=offload_min_bytes)
+                          stash_budget_bytes=stash_budget_bytes, offload_min_bytes=offload_min_bytes,
+                          regen_pre_x=regen_pre_x)
     else:
         model = DeviceModel.from_host(sched, params, range(sched.n_stages), device)
         rt = HelixRuntime(sched, model, mlp_chunk, "multistream" if threaded else "replay", device,
                           record_timeline=record_timeline, stash_budget_bytes=stash_budget_bytes,
-                          offload_min_bytes=offload_min_bytes)
+                          offload_min_bytes=offload_min_bytes, regen_pre_x=regen_pre_x)
     rt.run(_to_device_inputs(inputs, cfg, device))
     torch.cuda.synchronize()
     if dist:

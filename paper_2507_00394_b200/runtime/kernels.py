@@ -138,12 +138,25 @@ def attention_fwd(qkv, s: int, b: int, heads: int, o: torch.Tensor, lse: torch.T
     return o, lse
 
 
+def attention_delta(o, d_o, s: int, b: int, heads: int, delta: torch.Tensor):
+    """delta [b, heads, s] f32 = rowsum(d_o * o) per head (flash backward's D)."""
+    o, d_o = _rows(o), _rows(d_o)
+    if o.stride(0) != d_o.stride(0):
+        raise ValueError("o and d_o must share a row stride")
+    _need(delta, torch.float32, "delta")
+    _lib.call("hx_attn_bwd_delta", o.data_ptr(), d_o.data_ptr(), o.stride(0), delta.data_ptr(),
+              s, b, heads, o.shape[1] // heads, _stream())
+    return delta
+
+
 def attention_bwd(qkv, o, d_o, lse, s: int, b: int, heads: int, dqkv: torch.Tensor,
                   delta_ws: torch.Tensor, dq_ws: torch.Tensor):
+    """``o=None``: ``delta_ws`` already holds D (``attention_delta``)."""
     qkv = _rows(qkv)
     h = qkv.shape[1] // 3
-    _lib.call("hx_attn_bwd", qkv.data_ptr(), qkv.stride(0), o.data_ptr(), d_o.data_ptr(),
-              _rows(o).stride(0), lse.data_ptr(), delta_ws.data_ptr(), dq_ws.data_ptr(),
+    ld_o = _rows(d_o).stride(0) if o is None else _rows(o).stride(0)
+    _lib.call("hx_attn_bwd", qkv.data_ptr(), qkv.stride(0), None if o is None else o.data_ptr(),
+              d_o.data_ptr(), ld_o, lse.data_ptr(), delta_ws.data_ptr(), dq_ws.data_ptr(),
               dqkv.data_ptr(), _rows(dqkv).stride(0), s, b, heads, h // heads, _stream())
     return dqkv
 

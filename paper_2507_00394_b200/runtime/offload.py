@@ -64,7 +64,8 @@ class StashOffloader:
     """Budgeted stash residency for the stages one process executes."""
 
     def __init__(self, sched, stages: dict, weights: list[torch.Tensor], budget_bytes: int,
-                 min_bytes: int = 32 << 20):
+                 min_bytes: int = 32 << 20, regen_pre_x: bool = False):
+        self.regen_pre_x = regen_pre_x
         self.budget = int(budget_bytes)
         self.min_bytes = min_bytes
         self.weight_ptrs = {w.untyped_storage().data_ptr() for w in weights}
@@ -101,9 +102,11 @@ class StashOffloader:
 
     # -- schedule knowledge ---------------------------------------------------------------
 
-    @staticmethod
-    def consumed_keys(t) -> list[tuple]:
+    def consumed_keys(self, t) -> list[tuple]:
         if t.kind == RECOMPUTE:
+            if self.regen_pre_x and t.comp == "pre" and t.layer > 0:
+                # rc.pre(l) rebuilds x from post(l-1)'s retention (executor regen_pre_x)
+                return [(t.layer, t.mb, "pre"), (t.layer - 1, t.mb, "post")]
             return [(t.layer, t.mb, t.comp)]
         if t.kind == BWD_B:
             if t.comp == "chunk":

@@ -112,7 +112,7 @@ class CpuMath:
         slot += (z * z).sum()
         return z * (2.0 / z.numel())
 
-    def post_backward_b(self, d_out, W, G, st):
+    def post_backward_b(self, d_out, W, G, st, fuse_w=False):
         d_m1 = (d_out @ W["mlp_w2"].t()) * _gelu_grad(st["m1"])
         d_ln2 = d_m1 @ W["mlp_w1"].t()
         dx, dg, db = _ln_bwd(d_ln2, st["x2"], W["ln2_gain"])
@@ -175,4 +175,12 @@ class CpuMath:
             if self.qkv:
                 return {"x": kept["x"]}
             return {"x": kept["x"], "ln_out": _ln(kept["x"], W["ln1_gain"], W["ln1_bias"])}
+        if "_x2" in kept:
+            x2, ln2 = kept["_x2"], kept["_ln2_out"]
+            m1 = ln2 @ W["mlp_w1"]
+            return {"attn_out": kept["attn_out"], "x2": x2, "ln2_out": ln2, "m1": m1, "g": _gelu(m1)}
         return self._post_trunk(kept["attn_out"], kept["residual"], W)
+
+    def post_output(self, kept, W):
+        t = self._post_trunk(kept["attn_out"], kept["residual"], W)
+        return t["x2"] + t["g"] @ W["mlp_w2"], {"_x2": t["x2"], "_ln2_out": t["ln2_out"]}

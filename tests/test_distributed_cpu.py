@@ -47,7 +47,8 @@ def _worker(rank, world, port, cfg_kw, method, qkv, q, env=None):
                 layers[l] = DeviceLayer(t, own, grad_dtype=torch.float64)
         math = CpuMath(cfg, bool(int(sched.meta["qkv"])))
         rt = HelixRuntime(sched, DeviceModel(layers), None, "distributed", torch.device("cpu"),
-                          math=math, rank=rank, groups=pair_groups(world))
+                          math=math, rank=rank, groups=pair_groups(world),
+                          regen_pre_x=os.environ.get("HX_TEST_REGEN_PRE_X") == "1")
         inputs = [torch.from_numpy(x).reshape(cfg.s * cfg.b, cfg.h) for x in make_inputs(cfg, 1)]
         rt.run(inputs)
         stats = [rt.comm_stats]
@@ -166,3 +167,18 @@ def test_default_lookahead_bounds_transit():
         for st in per_iter:
             for peer, n in st["max_live_sends_per_peer"].items():
                 assert 1 <= n <= len(plan.send_seq[(rank, peer)])
+
+
+def test_regen_pre_x_two_and_four_ranks():
+    """SURVEY H1 step 1 over the distributed driver: the pre stash drops x and
+    rc.pre(l) rebuilds it from post(l-1)'s retention on the same rank."""
+    for world, toy in ((2, TOY2), (4, TOY4)):
+        losses, grads, peaks = run_world(world, toy, "helix_twofold_rc", env={"HX_TEST_REGEN_PRE_X": "1"})
+        ref = _oracle(toy)
+        assert np.allclose(losses, ref.losses, rtol=1e-10, atol=0)
+        for l in range(toy["L"]):
+            for k in O.FIELDS:
+                assert np.allclose(grads[l][k], ref.param_grads[l][k], rtol=1e-9, atol=1e-12), (world, l, k)
+        # the logical stash (reference keys) is unchanged
+        _, _, base_peaks = run_world(world, toy, "helix_twofold_rc")
+        assert peaks == base_peaks

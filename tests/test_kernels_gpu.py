@@ -72,6 +72,29 @@ def test_gemm_dw_split_k(M, N, Kd):
     assert rel_err(acc, want) < 1e-4
 
 
+@pytest.mark.parametrize("M,N,Kd", [(256, 1024, 100), (512, 2048, 36), (4096, 4096, 1000), (128, 64, 1)])
+def test_gemm_dw_ragged_k(M, N, Kd):
+    # weight gradient over a ragged MLP row slab (K not a multiple of 8): the
+    # K tail is read through TMA out-of-bounds zero fill
+    x, dy = rnd(Kd, M, seed=17), rnd(Kd, N, seed=18)
+    acc = torch.randn(M, N, device=DEV)
+    want = acc + x.float().t() @ dy.float()
+    K.linear_dw(x, dy, acc, accumulate=True)
+    torch.cuda.synchronize()
+    assert rel_err(acc, want) < 1e-4
+
+
+def test_attention_delta_matches_rowsum():
+    # D = rowsum(dO * O) per (batch, head, query), fp32
+    s, b, heads, d = 300, 2, 3, 64
+    o, do = rnd(s * b, heads * d, seed=19), rnd(s * b, heads * d, seed=20)
+    delta = torch.empty(b * heads * s, device=DEV)
+    K.attention_delta(o, do, s, b, heads, delta)
+    torch.cuda.synchronize()
+    want = (o.float() * do.float()).view(s, b, heads, d).sum(-1).permute(1, 2, 0).reshape(-1)
+    assert rel_err(delta, want) < 1e-5
+
+
 def test_gemm_epilogues():
     T, Kd, N = 512, 256, 1024
     x, w = rnd(T, Kd, seed=7), rnd(Kd, N, scale=Kd ** -0.5, seed=8)

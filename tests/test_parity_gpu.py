@@ -124,3 +124,37 @@ def test_reports_stall():
     sched.per_stage_order[0].reverse()
     with pytest.raises(StalledSchedule):
         execute_schedule(sched, make_model(SMALL, 0), make_inputs(SMALL, 1))
+
+
+@pytest.mark.parametrize("qkv", [True, False])
+def test_regen_pre_x_matches_oracle(qkv):
+    """pre stashes drop x; rc.pre(l) rebuilds it from
+    post(l-1)'s retention (two extra MLP GEMMs) -- same numbers, ragged slabs."""
+    for cfg, chunk in ((SMALL, 100), (WIDE, None)):
+        sched = generate("helix_twofold_rc", cfg, UNIT, qkv_in_attention=qkv)
+        res = execute_schedule(sched, make_model(cfg, 0), make_inputs(cfg, 1), mlp_chunk=chunk,
+                               regen_pre_x=True)
+        compare(res, oracle_for(cfg), cfg.L, f"regen_pre_x qkv={qkv} chunk={chunk}")
+
+
+@pytest.mark.parametrize("method,chunk,regen", [("helix_twofold", None, False), ("helix_twofold_rc", 64, False),
+                                                ("helix_twofold_rc", 100, True), ("1f1b_rc", 64, False),
+                                                ("zb1p", None, False)])
+def test_device_stash_bytes_match_memplan(method, chunk, regen):
+    """runtime/memplan.stash_walk with the LayerMath tensor set (bf16, fp32 LSE,
+    per-slab m1/g, no stashed O) equals the distinct device bytes the executor
+    holds, at p = 1 (one stage per process: the same sharing as one rank)."""
+    from paper_2507_00394_b200.runtime import HelixRuntime
+    from paper_2507_00394_b200.runtime.executor import DeviceModel
+    from paper_2507_00394_b200.runtime.memplan import stash_walk
+    cfg = ModelConfig(L=4, h=128, s=256, b=1, num_heads=2, p=1, m=2)
+    sched = generate(method, cfg, UNIT)
+    dev = torch.device("cuda", 0)
+    model = DeviceModel.from_host(sched, make_model(cfg, 0), [0], dev)
+    rt = HelixRuntime(sched, model, chunk, "replay", dev, regen_pre_x=regen)
+    inputs = [torch.from_numpy(x).to(dev, torch.bfloat16).reshape(cfg.s * cfg.b, cfg.h)
+              for x in make_inputs(cfg, 1)]
+    rt.run(inputs)
+    torch.cuda.synchronize()
+    want, at = stash_walk(sched, 0, regen_pre_x=regen)
+    assert rt.stages[0].peak_bytes == want, (rt.stages[0].peak_bytes, rt.stages[0].peak_bytes_at, want, at)

@@ -206,6 +206,214 @@ __global__ void __launch_bounds__(256) ln_bwd_dgdb_kernel(const __nv_bfloat16* _
   }
 }
 
+// ------------------------------------------------------------------ LayerNorm v2
+// Column-sliced blocks (round 2).  A block of 8 warps owns a contiguous range of
+// rows and walks it R rows at a time; lane (w, l) owns the 16-byte column
+// vectors (32w + l) + 256i, i < VPL, so every warp reads whole 512-byte
+// segments of a row and each thread's LayerNorm gain / bias (and, backward,
+// its gain / bias gradient partials) stay in registers for the whole block.
+// Per-row statistics are combined across the 8 warps through shared memory.
+// Each row is read from HBM exactly once (the row-per-warp v1 re-read it for
+// the second pass), and the backward fuses the gain / bias column reduction
+// (v1 re-read dy and x in a second kernel): LN forward moves 2*T*h*2 bytes and
+// LN backward 4*T*h*2 (dy, x, dres in; dx out), the algorithmic minimum.
+template <int VPL, int R, int MINB>
+__global__ void __launch_bounds__(256, MINB) ln_fwd_v2_kernel(const __nv_bfloat16* __restrict__ x,
+                                                         const float* __restrict__ gain,
+                                                         const float* __restrict__ bias,
+                                                         __nv_bfloat16* __restrict__ y, int rows, int h,
+                                                         int rows_per_block) {
+  __shared__ float2 part[2][R][8];
+  const int lane = lane_id(), w = warp_id();
+  const int nvec = h / 8;
+  const int base = 32 * w + lane;
+  float g[VPL][8], bb[VPL][8];
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int c = base + 256 * i;
+    if (c < nvec) {
+      load_gain8(gain, c, g[i]);
+      load_gain8(bias, c, bb[i]);
+    }
+  }
+  const int r_begin = blockIdx.x * rows_per_block;
+  const int r_end = min(rows, r_begin + rows_per_block);
+  int buf = 0;
+  for (int r0 = r_begin; r0 < r_end; r0 += R, buf ^= 1) {
+    uint4 u[R][VPL];
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        const int c = base + 256 * i;
+        if (r0 + j < r_end && c < nvec)
+          u[j][i] = __ldcs(reinterpret_cast<const uint4*>(x + static_cast<int64_t>(r0 + j) * h) + c);
+        else
+          u[j][i] = make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      float sum = 0.f, sq = 0.f;
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        float f[8];
+        unpack8(u[j][i], f);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          sum += f[k];
+          sq = fmaf(f[k], f[k], sq);
+        }
+      }
+      sum = warp_sum(sum);
+      sq = warp_sum(sq);
+      if (lane == 0) part[buf][j][w] = make_float2(sum, sq);
+    }
+    // double-buffered partials: one barrier per batch (the next batch writes the other buffer)
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      if (r0 + j >= r_end) break;
+      float sum = 0.f, sq = 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float2 t = part[buf][j][k];
+        sum += t.x;
+        sq += t.y;
+      }
+      const float mu = sum / h;
+      const float rstd = rsqrtf(fmaxf(sq / h - mu * mu, 0.f) + LN_EPS);
+      uint4* yr = reinterpret_cast<uint4*>(y + static_cast<int64_t>(r0 + j) * h);
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        const int c = base + 256 * i;
+        if (c < nvec) {
+          float f[8], o[8];
+          unpack8(u[j][i], f);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) o[k] = (f[k] - mu) * rstd * g[i][k] + bb[i][k];
+          yr[c] = make_uint4(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]), pack_bf16(o[4], o[5]),
+                             pack_bf16(o[6], o[7]));
+        }
+      }
+    }
+  }
+}
+
+template <int VPL, int R, int MINB>
+__global__ void __launch_bounds__(256, MINB) ln_bwd_v2_kernel(
+    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x, const float* __restrict__ gain,
+    const __nv_bfloat16* __restrict__ dres, __nv_bfloat16* __restrict__ dx, float* __restrict__ dgain,
+    float* __restrict__ dbias, int rows, int h, int rows_per_block) {
+  __shared__ float4 part[2][R][8];
+  const int lane = lane_id(), w = warp_id();
+  const int nvec = h / 8;
+  const int base = 32 * w + lane;
+  float g[VPL][8], adg[VPL][8], adb[VPL][8];
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int c = base + 256 * i;
+    if (c < nvec) load_gain8(gain, c, g[i]);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) adg[i][k] = adb[i][k] = 0.f;
+  }
+  const int r_begin = blockIdx.x * rows_per_block;
+  const int r_end = min(rows, r_begin + rows_per_block);
+  int buf = 0;
+  for (int r0 = r_begin; r0 < r_end; r0 += R, buf ^= 1) {
+    uint4 ux[R][VPL], ud[R][VPL];
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        const int c = base + 256 * i;
+        const int64_t off = static_cast<int64_t>(r0 + j) * h;
+        if (r0 + j < r_end && c < nvec) {
+          ux[j][i] = __ldcs(reinterpret_cast<const uint4*>(x + off) + c);
+          ud[j][i] = __ldcs(reinterpret_cast<const uint4*>(dy + off) + c);
+        } else {
+          ux[j][i] = ud[j][i] = make_uint4(0, 0, 0, 0);
+        }
+      }
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      float sx = 0.f, sxx = 0.f, sg = 0.f, sgx = 0.f;
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        float f[8], d[8];
+        unpack8(ux[j][i], f);
+        unpack8(ud[j][i], d);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float gd = d[k] * g[i][k];
+          sx += f[k];
+          sxx = fmaf(f[k], f[k], sxx);
+          sg += gd;
+          sgx = fmaf(gd, f[k], sgx);
+        }
+      }
+      sx = warp_sum(sx);
+      sxx = warp_sum(sxx);
+      sg = warp_sum(sg);
+      sgx = warp_sum(sgx);
+      if (lane == 0) part[buf][j][w] = make_float4(sx, sxx, sg, sgx);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      if (r0 + j >= r_end) break;
+      float4 t = part[buf][j][0];
+#pragma unroll
+      for (int k = 1; k < 8; ++k) {
+        const float4 q = part[buf][j][k];
+        t.x += q.x;
+        t.y += q.y;
+        t.z += q.z;
+        t.w += q.w;
+      }
+      const float mu = t.x / h;
+      const float rstd = rsqrtf(fmaxf(t.y / h - mu * mu, 0.f) + LN_EPS);
+      const float m1 = t.z / h;                       // mean(dxhat)
+      const float m2 = (t.w / h - mu * m1) * rstd;    // mean(dxhat * xhat)
+      const int64_t off = static_cast<int64_t>(r0 + j) * h;
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        const int c = base + 256 * i;
+        if (c < nvec) {
+          float f[8], d[8], o[8];
+          unpack8(ux[j][i], f);
+          unpack8(ud[j][i], d);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const float xh = (f[k] - mu) * rstd;
+            o[k] = rstd * (d[k] * g[i][k] - m1) - xh * rstd * m2;
+            adg[i][k] = fmaf(d[k], xh, adg[i][k]);
+            adb[i][k] += d[k];
+          }
+          if (dres) {
+            float r[8];
+            unpack8(__ldcs(reinterpret_cast<const uint4*>(dres + off) + c), r);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) o[k] += r[k];
+          }
+          reinterpret_cast<uint4*>(dx + off)[c] = make_uint4(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]),
+                                                             pack_bf16(o[4], o[5]), pack_bf16(o[6], o[7]));
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int c = base + 256 * i;
+    if (c < nvec && r_begin < r_end) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        atomicAdd(&dgain[8 * c + k], adg[i][k]);
+        atomicAdd(&dbias[8 * c + k], adb[i][k]);
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) mse_loss_kernel(const __nv_bfloat16* __restrict__ z, int64_t n,
                                                         __nv_bfloat16* __restrict__ dz,
                                                         double* __restrict__ sumsq) {
@@ -280,8 +488,62 @@ static int ln_grid(int per_sm, int rows) {
   return blocks < resident ? blocks : resident;
 }
 
+// LN v2 (default) / v1 (HX_LN=1, kept for A/B runs).
+static int ln_version() {
+  static const int v = getenv("HX_LN") ? atoi(getenv("HX_LN")) : 2;
+  return v;
+}
+// (2: 2 blocks of 8 warps per SM, small row batches; 3: 1 block, larger batches)
+
+// Persistent grid for the v2 kernels: the blocks that fit at once, each owning
+// an equal contiguous share of the rows (a multiple of R).
+template <typename K>
+static void ln_v2_grid(K kernel, int rows, int R, int* grid, int* per_block) {
+  static int per_sm_cache = 0;
+  (void)per_sm_cache;
+  const int per_sm = ln_blocks_per_sm(kernel);
+  int blocks = num_sms() * per_sm;
+  const int batches = (rows + R - 1) / R;
+  if (blocks > batches) blocks = batches;
+  const int per = (batches + blocks - 1) / blocks;
+  *per_block = per * R;
+  *grid = (rows + *per_block - 1) / *per_block;
+}
+
+// (VPL, R) per width: R rows per batch keep the row data of a batch (R * VPL
+// 16-byte vectors per tensor and lane) in registers without spills at 2
+// blocks per SM (ptxas -v: no stack for any instance)
+#define HX_VPL_DISPATCH(h, F, R1, R2, R4)    \
+  do {                                       \
+    const int vpl_ = ((h) / 8 + 255) / 256;  \
+    if (vpl_ <= 1) { F(1, R1); }             \
+    else if (vpl_ <= 2) { F(2, R2); }        \
+    else if (vpl_ <= 4) { F(4, R4); }        \
+    else return cudaErrorInvalidValue;       \
+  } while (0)
+
 cudaError_t ln_fwd_launch(const void* x, const float* g, const float* b, void* y, int rows, int h,
                           cudaStream_t st) {
+  if (ln_version() >= 2) {
+#define LF(VPL, R, MB)                                                                                    \
+  {                                                                                                       \
+    int grid, per;                                                                                        \
+    ln_v2_grid(ln_fwd_v2_kernel<VPL, R, MB>, rows, R, &grid, &per);                                       \
+    ln_fwd_v2_kernel<VPL, R, MB><<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), g, b,         \
+                                                       static_cast<__nv_bfloat16*>(y), rows, h, per);    \
+  }
+#define L2(VPL, R) LF(VPL, R, 2)
+#define L3(VPL, R) LF(VPL, R, 1)
+    if (ln_version() == 3) {
+      HX_VPL_DISPATCH(h, L3, 8, 4, 2);
+    } else {
+      HX_VPL_DISPATCH(h, L2, 8, 4, 1);
+    }
+#undef L2
+#undef L3
+#undef LF
+    return cudaGetLastError();
+  }
 #define L(NV)                                                                          \
   static const int per_sm_##NV = ln_blocks_per_sm(ln_fwd_kernel<NV>);                    \
   ln_fwd_kernel<NV><<<ln_grid(per_sm_##NV, rows), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), g, b, \
@@ -293,6 +555,27 @@ cudaError_t ln_fwd_launch(const void* x, const float* g, const float* b, void* y
 
 cudaError_t ln_bwd_launch(const void* dy, const void* x, const float* g, const void* dres, void* dx,
                           float* dg, float* db, float* stats, int rows, int h, cudaStream_t st) {
+  if (ln_version() >= 2) {
+#define LB(VPL, R, MB)                                                                                      \
+  {                                                                                                         \
+    int grid, per;                                                                                          \
+    ln_v2_grid(ln_bwd_v2_kernel<VPL, R, MB>, rows, R, &grid, &per);                                         \
+    ln_bwd_v2_kernel<VPL, R, MB><<<grid, 256, 0, st>>>(                                                     \
+        static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), g,                     \
+        static_cast<const __nv_bfloat16*>(dres), static_cast<__nv_bfloat16*>(dx), dg, db, rows, h, per);    \
+  }
+#define L2(VPL, R) LB(VPL, R, 2)
+#define L3(VPL, R) LB(VPL, R, 1)
+    if (ln_version() == 3) {
+      HX_VPL_DISPATCH(h, L3, 8, 4, 2);
+    } else {
+      HX_VPL_DISPATCH(h, L2, 4, 2, 1);
+    }
+#undef L2
+#undef L3
+#undef LB
+    return cudaGetLastError();
+  }
   float2* st2 = reinterpret_cast<float2*>(stats);
 #define L(NV)                                                                                   \
   static const int per_sm_##NV = ln_blocks_per_sm(ln_bwd_dx_kernel<NV>);                         \

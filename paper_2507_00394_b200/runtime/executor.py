@@ -98,8 +98,9 @@ class _Stage:
         self.wctx: dict[int, list] = {}
         self.peak = 0
         self.ln_wctx_elements = ln_wctx_elements
-        # device bytes of the distinct tensors held by stash + W contexts (weights
-        # and inputs excluded), after each task: checked against runtime/memplan.py
+        # device bytes of the distinct tensors held by stash, W contexts and
+        # stage-local payloads (weights and inputs excluded), after each task:
+        # checked against runtime/memplan.py
         self.peak_bytes = 0
         self.peak_bytes_at = ""
         self.resident_ptrs: set[int] = set()
@@ -116,6 +117,8 @@ class _Stage:
                         seen[ptr] = st.nbytes()
 
         for e in self.stash.values():
+            visit(e)
+        for e in self.values.values():
             visit(e)
         for lst in self.wctx.values():
             for _l, w_post, w_pre in lst:
@@ -179,6 +182,89 @@ class DeviceModel:
             dl.zero_grads(zero_fn)
 
 
+class HostInput:
+    """Stash placeholder for a micro-batch input (layer 0's x) that stays in
+    host memory while the input streamer is active; counted like the tensor
+    (``numel``) and copied back to the device by the task that reads it."""
+
+    __slots__ = ("mb", "n")
+
+    def __init__(self, mb: int, n: int):
+        self.mb = mb
+        self.n = n
+
+    def numel(self) -> int:
+        return self.n
+
+
+class _InputStreamer:
+    """Micro-batch inputs kept in (pinned) host memory and copied to the device
+    just before the tasks that read them: layer 0's forward, and its recompute
+    / backward (LayerNorm-1 backward needs x), on a side stream a few tasks
+    ahead (``lookahead``) so the copy overlaps compute.  The device copy lives
+    only as long as those tasks' payloads and stashes hold it, so a stage never
+    keeps all m inputs resident (16 GB on stage 0 at 7B/128k)."""
+
+    def __init__(self, sched: Schedule, stages: dict, host: list, device, lookahead: int = 3):
+        self.host = host
+        self.device = device
+        self.cuda = device.type == "cuda"
+        self.stream = torch.cuda.Stream(device=device) if self.cuda else None
+        self.lookahead = lookahead
+        self.ready: dict[str, tuple] = {}
+        self.uses: dict[int, list[tuple[int, str, int]]] = {}
+        self.pos: dict[str, int] = {}
+        for si in stages:
+            seen_bwd: set[int] = set()
+            lst = []
+            for pos, tid in enumerate(sched.per_stage_order[si]):
+                t = sched.tasks[tid]
+                self.pos[tid] = pos
+                if t.layer != 0 or t.kind not in (FWD, RECOMPUTE, BWD_B) or t.comp not in ("pre", "chunk"):
+                    continue
+                if t.kind == FWD:
+                    lst.append((pos, tid, t.mb))
+                elif t.mb not in seen_bwd:      # the first of rc.pre.l0 / b.pre.l0 (or the chunk bwd)
+                    seen_bwd.add(t.mb)
+                    lst.append((pos, tid, t.mb))
+            self.uses[si] = lst
+        self.h2d_bytes = 0
+
+    def _issue(self, tid: str, mb: int) -> None:
+        if tid in self.ready:
+            return
+        src = self.host[mb]
+        if not self.cuda:
+            self.ready[tid] = (src.clone(), None)
+            return
+        cur = torch.cuda.current_stream(self.device)
+        self.stream.wait_stream(cur)          # the buffer's allocation is ordered
+        with torch.cuda.stream(self.stream):
+            dev = torch.empty(src.shape, dtype=src.dtype, device=self.device)
+            dev.copy_(src, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+        self.ready[tid] = (dev, ev)
+        self.h2d_bytes += src.numel() * src.element_size()
+
+    def before_task(self, si: int, tid: str) -> None:
+        pos = self.pos.get(tid)
+        if pos is None:
+            return
+        for p, use, mb in self.uses.get(si, ()):
+            if pos <= p < pos + self.lookahead:
+                self._issue(use, mb)
+
+    def get(self, tid: str, mb: int) -> torch.Tensor:
+        self._issue(tid, mb)
+        dev, ev = self.ready.pop(tid)
+        if ev is not None:
+            cur = torch.cuda.current_stream(self.device)
+            cur.wait_event(ev)
+            dev.record_stream(cur)
+        return dev
+
+
 class _Core:
     """Task interpreter shared by the drivers (``executor.py:136-293``)."""
 
@@ -199,6 +285,7 @@ class _Core:
         # from post(l-1)'s retention on the same stage (HelixRuntime.regen_pre_x)
         self.regen_pre_x = False
         self.inputs: list[torch.Tensor] = []
+        self.streamer: _InputStreamer | None = None    # host-resident inputs (HelixRuntime.run)
         self.recv_of_send = {t.deps[0]: t.id for t in self.tasks.values() if t.kind == RECV}
         self.sends_by_producer: dict[str, list[Task]] = {}
         for t in self.tasks.values():
@@ -254,8 +341,27 @@ class _Core:
 
     # -- compute tasks ------------------------------------------------------------------
 
+    def input_x(self, t: Task) -> torch.Tensor:
+        """Layer 0's input for ``t``'s micro-batch (device tensor)."""
+        if self.streamer is not None:
+            return self.streamer.get(t.id, t.mb)
+        return self.inputs[t.mb]
+
+    def _keep_x(self, stash: dict, mb: int) -> dict:
+        """With streamed inputs the layer-0 pre stash keeps a host placeholder."""
+        if self.streamer is not None and isinstance(stash.get("x"), torch.Tensor):
+            stash = dict(stash)
+            stash["x"] = HostInput(mb, int(stash["x"].numel()))
+        return stash
+
+    def _fetch_x(self, stash: dict | None, t: Task) -> None:
+        if stash is not None and isinstance(stash.get("x"), HostInput):
+            stash["x"] = self.streamer.get(t.id, t.mb)
+
     def run_compute(self, t: Task) -> None:
         st = self.stages[t.stage]
+        if self.streamer is not None:
+            self.streamer.before_task(t.stage, t.id)
         if self.offload is not None:
             self.offload.before_task(st, t)
         self._run_compute(st, t)
@@ -274,6 +380,8 @@ class _Core:
                 self.math.pre_backward_w(w_pre, self.G(l))
         elif t.kind == RECOMPUTE:
             key = (t.layer, t.mb, t.comp)
+            if t.comp == "pre" and t.layer == 0:
+                self._fetch_x(st.stash.get(key), t)
             if self.regen_pre_x and t.comp == "pre" and t.layer > 0:
                 # post(l-1) runs on this stage (pre_stage(l) == post_stage(l-1),
                 # P/partition.py:25-36) and its rc.post comes after this task
@@ -293,8 +401,10 @@ class _Core:
     def _fwd_component(self, st: _Stage, t: Task) -> None:
         src = self.input_id(t)
         if t.comp == "pre":
-            x = self.inputs[t.mb] if src is None else self.take(st, src)["x"]
+            x = self.input_x(t) if src is None else self.take(st, src)["x"]
             payload, full = self.math.pre_forward(x, self.W(t.layer))
+            if t.layer == 0:
+                full = self._keep_x(full, t.mb)
             self.store_stash(st, t.layer, t.mb, "pre", full, {})
             st.values[t.id] = payload
         elif t.comp == "attn":
@@ -326,15 +436,18 @@ class _Core:
         else:
             payload = self.take(st, src)
             stash = st.stash.pop((l, t.mb, "pre"))
+            self._fetch_x(stash, t)
             d_x = self.math.pre_backward(payload, self.W(l), self.G(l), stash)
             if l > 0:
                 st.values[t.id] = {"d_x": d_x}
 
     def _fwd_chunk(self, st: _Stage, t: Task) -> None:
         src = self.input_id(t)
-        x = self.inputs[t.mb] if src is None else self.take(st, src)["x"]
+        x = self.input_x(t) if src is None else self.take(st, src)["x"]
         for l in range(t.layer, t.layer + t.span):
             pa, s_pre = self.math.pre_forward(x, self.W(l))
+            if l == 0:
+                s_pre = self._keep_x(s_pre, t.mb)
             self.store_stash(st, l, t.mb, "pre", s_pre, {})
             ap, s_attn = self.math.attn_forward(pa)
             self.store_stash(st, l, t.mb, "attn", s_attn, pa)
@@ -354,6 +467,8 @@ class _Core:
             s_post = st.stash.pop((l, t.mb, "post"))
             s_attn = st.stash.pop((l, t.mb, "attn"))
             s_pre = st.stash.pop((l, t.mb, "pre"))
+            if l == 0:
+                self._fetch_x(s_pre, t)
             if self.rc:  # 1f1b_rc: regenerate this layer's non-attention stash in place
                 s_post = self.math.regenerate_stash("post", s_post, W)
                 s_pre = self.math.regenerate_stash("pre", s_pre, W)
@@ -748,6 +863,63 @@ class _Distributed:
         return {peer: q.max_live for peer, q in self.sends.items()}
 
 
+class _Loopback:
+    """Stage probe: rank ``rank``'s tasks of a p-stage schedule alone on this
+    GPU, with no peers.  Each RECV is satisfied just before its consumer by a
+    freshly allocated payload of the wire layout (``_payload_layout``: the
+    same buffers a real receive allocates), filled with synthetic values
+    (N(0, 1) activations, N(0, 1e-3) gradients, N(0, 1/h) weights); each
+    SEND's payload is checked against ``comm_volume`` and dropped (``send_cap``
+    > 0 keeps that many per peer, the distributed driver's bound; how long a
+    real send stays outstanding depends on its receiver, which the memory plan
+    models on a timeline instead).  Compute runs the product kernels at the real per-stage shapes, so
+    one B200 measures a rank's device memory and busy time for a p = 2..8
+    pipeline it cannot otherwise host (memory plan validation)."""
+
+    def __init__(self, core: _Core, rank: int, send_cap: int = 0, seed: int = 7):
+        self.core = core
+        self.rank = rank
+        self.send_cap = send_cap
+        st = core.stages[rank]
+        self.gen = torch.Generator(device=st.device).manual_seed(seed)
+        order = core.sched.per_stage_order[rank]
+        self.needs: list[list[str]] = []
+        seen: set[str] = set()
+        for tid in order:
+            t = core.tasks[tid]
+            need = [d for d in t.deps if d not in seen and (dt := core.tasks.get(d)) is not None
+                    and dt.kind == RECV and dt.stage == rank]
+            seen.update(need)
+            self.needs.append(need)
+
+    def _fake(self, rid: str) -> dict:
+        core, cfg = self.core, self.core.cfg
+        dev = core.stages[self.rank].device
+        out = {}
+        for name, shape, dtype in _payload_layout(cfg, _edge_tag(rid), core.qkv, core.math):
+            buf = torch.empty(shape, dtype=dtype, device=dev)
+            scale = (cfg.h ** -0.5) if name == "qkv_weight" else \
+                (1e-3 if name.startswith("d_") or name == "delta" else 1.0)
+            buf.normal_(0.0, scale, generator=self.gen)
+            out[name] = buf
+        return out
+
+    def run(self, timer: _Timer) -> None:
+        core, r = self.core, self.rank
+        st = core.stages[r]
+        inflight: dict[int, deque] = {}
+        for k, tid in enumerate(core.sched.per_stage_order[r]):
+            for d in self.needs[k]:
+                st.values[d] = self._fake(d)
+            with timer.around(tid):
+                core.run_compute(core.tasks[tid])
+            for snd in core.sends_by_producer.get(tid, ()):
+                q = inflight.setdefault(snd.peer, deque())
+                q.append(core.checked_payload(snd))
+                while len(q) > self.send_cap:
+                    q.popleft()
+
+
 def make_pair_groups(n_stages: int, warm: bool = True, device=None) -> dict[tuple[int, int], object]:
     """One 2-rank group per directed stage pair; every rank must call this in
     the same order (``torch.distributed.new_group`` is collective).
@@ -815,8 +987,9 @@ class HelixRuntime:
                  mode: str = "replay", device=None, math=None, rank: int | None = None,
                  groups: dict | None = None, record_timeline: bool = False,
                  stash_budget_bytes: int | None = None, offload_min_bytes: int = 32 << 20,
-                 regen_pre_x: bool = False):
+                 regen_pre_x: bool = False, stream_inputs: bool = False):
         self.sched = sched
+        self.stream_inputs = stream_inputs
         self.cfg = meta_config(sched)
         self.mode = mode
         self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -826,7 +999,7 @@ class HelixRuntime:
             defer_w=sched.meta.get("backward") == "split")
         self.model = model
         self.rank = rank
-        local = [rank] if mode == "distributed" else list(range(sched.n_stages))
+        local = [rank] if mode in ("distributed", "probe") else list(range(sched.n_stages))
         ln_ctx = self.cfg.s * self.cfg.b * self.cfg.h
         self.stages = {si: _Stage(si, self.device, None, ln_ctx) for si in local}
         self.sumsq = torch.zeros(self.cfg.m, dtype=torch.float64, device=self.device)
@@ -858,11 +1031,18 @@ class HelixRuntime:
         cfg = self.cfg
         if len(inputs) != cfg.m:
             raise ExecutionError(f"need {cfg.m} input microbatches, got {len(inputs)}")
-        self.core.inputs = [x.reshape(cfg.s * cfg.b, cfg.h) for x in inputs]
-        if self.core.offload is not None:
-            self.core.offload.exclude(self.core.inputs)
+        # (a stage probe of a rank that never reads the inputs may pass None)
+        self.core.inputs = [None if x is None else x.reshape(cfg.s * cfg.b, cfg.h) for x in inputs]
+        # host inputs on a CUDA runtime (or stream_inputs): copied in per task, never all resident
+        host = any(x is not None and x.device.type == "cpu" for x in self.core.inputs) and \
+            self.device.type == "cuda"
+        self.core.streamer = _InputStreamer(self.sched, self.stages, self.core.inputs, self.device) \
+            if (host or self.stream_inputs) else None
+        if self.core.offload is not None and self.core.streamer is None:
+            self.core.offload.exclude([x for x in self.core.inputs if x is not None])
         resident = {w.untyped_storage().data_ptr() for dl in self.model.layers.values() for w in dl.w.values()}
-        resident |= {x.untyped_storage().data_ptr() for x in self.core.inputs}
+        if self.core.streamer is None:
+            resident |= {x.untyped_storage().data_ptr() for x in self.core.inputs if x is not None}
         for st in self.stages.values():
             st.peak = 0
             st.peak_bytes, st.peak_bytes_at = 0, ""
@@ -884,6 +1064,8 @@ class HelixRuntime:
             self.comm_stats = {"max_live_sends_per_peer": drv.max_live_sends,
                                "recv_ahead": drv.recv_ahead, "send_cap": drv.send_cap,
                                "stash_peak_bytes": st.peak_bytes, "stash_peak_at": st.peak_bytes_at}
+        elif self.mode == "probe":
+            _Loopback(self.core, self.rank).run(timer)
         else:
             raise ExecutionError(f"unknown mode {self.mode!r}")
         self.timeline = timer.collect()
@@ -917,21 +1099,28 @@ class HelixRuntime:
                 for l, dl in self.model.layers.items()}
 
 
-def _to_device_inputs(inputs, cfg, device) -> list[torch.Tensor]:
+def _to_device_inputs(inputs, cfg, device, stream: bool = False) -> list[torch.Tensor]:
+    """bf16 ``[s*b, h]`` inputs: on ``device``, or (``stream``) in pinned host
+    memory for the runtime's input streamer.  Input tensors already on the
+    device stay there."""
     out = []
     for i, x in enumerate(inputs):
         shape = tuple(x.shape)
         if shape != (cfg.s, cfg.b, cfg.h):
             raise ExecutionError(f"input {i} has shape {shape}, want {(cfg.s, cfg.b, cfg.h)}")
         t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))
-        out.append(t.to(device=device, dtype=torch.bfloat16).reshape(cfg.s * cfg.b, cfg.h).contiguous())
+        if stream and t.device.type == "cpu":
+            out.append(t.to(dtype=torch.bfloat16).reshape(cfg.s * cfg.b, cfg.h).contiguous().pin_memory())
+        else:
+            out.append(t.to(device=device, dtype=torch.bfloat16).reshape(cfg.s * cfg.b, cfg.h).contiguous())
     return out
 
 
 def execute_schedule(sched: Schedule, params: list[LayerParams], inputs: list,
                      mlp_chunk: int | None = None, threaded: bool = False,
                      record_timeline: bool = False, *, stash_budget_bytes: int | None = None,
-                     offload_min_bytes: int = 32 << 20, regen_pre_x: bool = False) -> RunResult:
+                     offload_min_bytes: int = 32 << 20, regen_pre_x: bool = False,
+                     stream_inputs: bool = True) -> RunResult:
     """Run ``sched`` numerically on the B200(s); same contract as the reference.
 
     ``threaded=False``: replay on the current GPU.  ``threaded=True``: one rank
@@ -948,6 +1137,11 @@ def execute_schedule(sched: Schedule, params: list[LayerParams], inputs: list,
     ``x``; ``rc.pre(l)`` rebuilds it from ``post(l-1)``'s retention on the same
     stage, trading two MLP GEMMs per (layer, micro-batch)
     for ``b*s*h`` of stash.
+
+    ``stream_inputs`` (default): host inputs (NumPy, as the reference passes
+    them) stay in pinned host memory and are copied to the device per
+    micro-batch right before layer 0's forward and backward; False copies all
+    of them to the device up front.
     """
     cfg = meta_config(sched)
     if len(params) != cfg.L:
@@ -971,7 +1165,7 @@ def execute_schedule(sched: Schedule, params: list[LayerParams], inputs: list,
         rt = HelixRuntime(sched, model, mlp_chunk, "multistream" if threaded else "replay", device,
                           record_timeline=record_timeline, stash_budget_bytes=stash_budget_bytes,
                           offload_min_bytes=offload_min_bytes, regen_pre_x=regen_pre_x)
-    rt.run(_to_device_inputs(inputs, cfg, device))
+    rt.run(_to_device_inputs(inputs, cfg, device, stream=stream_inputs))
     torch.cuda.synchronize()
     if dist:
         return _gather_distributed(rt, params)

@@ -40,6 +40,7 @@ class Dtypes:
     wgrad: int = 4      # fp32 gradient accumulators and the shipped d_qkv_weight
     weight: int = 2     # bf16 weight matrices
     lse: int = 4        # per-row softmax statistics kept by the attention stash (0: none)
+    delta: int = 4      # flash D shipped in the gap payload (0: not shipped)
     slab_mlp: bool = True   # m1 / g regenerated per row slab (LayerMath); False: whole
 
 
@@ -75,9 +76,12 @@ def _is_chunked(sched: Schedule) -> bool:
 
 
 def stash_walk(sched: Schedule, stage: int, dt: Dtypes = Dtypes(), regen_pre_x: bool = False,
-               with_trace: bool = False):
+               with_trace: bool = False, stream_inputs: bool = False):
     """(peak bytes, task id at the peak[, per-task trace]) of the distinct
-    stash + deferred-W-context tensors alive on ``stage`` after each task."""
+    tensors held on ``stage`` after each task: stash, deferred W contexts and
+    stage-local payloads (produced, not yet consumed or sent).  With
+    ``stream_inputs`` layer 0's x is a device copy of a host input (counted)
+    that its pre stash does not keep (executor ``_InputStreamer``)."""
     cfg = _cfg(sched)
     qkv = bool(int(sched.meta.get("qkv", 0)))
     rc = bool(int(sched.meta.get("recompute", 0)))
@@ -106,8 +110,8 @@ def stash_walk(sched: Schedule, stage: int, dt: Dtypes = Dtypes(), regen_pre_x: 
             if refs[ident] == 0:
                 del refs[ident], sizes[ident]
 
-    def x_of(l, i):          # a layer input: the micro-batch input for l = 0 (resident anyway)
-        return (f"x:{l}.{i}", 0 if l == 0 else act)
+    def x_of(l, i):          # a layer input: the micro-batch input for l = 0 (resident, unless streamed)
+        return (f"x:{l}.{i}", 0 if (l == 0 and not stream_inputs) else act)
 
     def stage_of(comp, l, i):
         if chunked:
@@ -121,7 +125,7 @@ def stash_walk(sched: Schedule, stage: int, dt: Dtypes = Dtypes(), regen_pre_x: 
 
     def fwd(comp, l, i):
         if comp == "pre":
-            x = [] if (rc and regen_pre_x and l > 0) else [x_of(l, i)]
+            x = [] if ((rc and regen_pre_x and l > 0) or (stream_inputs and l == 0)) else [x_of(l, i)]
             if not qkv and not rc:
                 x.append((f"ln:{l}.{i}", act))
             hold((l, i, "pre"), x)
@@ -152,6 +156,8 @@ def stash_walk(sched: Schedule, stage: int, dt: Dtypes = Dtypes(), regen_pre_x: 
 
     def regen(comp, l, i):
         if comp == "pre":
+            if stream_inputs and l == 0:
+                hold((l, i, "pre"), [x_of(l, i)])
             if regen_pre_x and l > 0:
                 hold((l, i, "pre"), [(f"x:{l}.{i}", act)])
                 hold((l - 1, i, "post"), [(f"x2:{l - 1}.{i}", act), (f"ln2:{l - 1}.{i}", act)])
@@ -172,10 +178,69 @@ def stash_walk(sched: Schedule, stage: int, dt: Dtypes = Dtypes(), regen_pre_x: 
             [(f"ln:{l}.{i}", act), (f"dqkv:{l}.{i}", 3 * act)]
         return post + pre
 
+    # --- stage-local payloads (the executor's ``values``): a task's output is
+    # held from its end until its same-stage consumer runs, or -- if it is
+    # sent -- only at its own end (the drivers pop it right after the task)
+    L = cfg.L
+    dlt = cfg.b * cfg.num_heads * cfg.s * dt.delta
+    sent = {t.deps[0] for t in sched.tasks.values() if t.kind == "SEND"}
+    deps_of = {tid: set(sched.tasks[tid].deps) for tid in sched.per_stage_order[stage]}
+
+    def producer_of(t):
+        """Mirror of executor._Core.input_id for a local producer (None: an
+        input, a received payload, or nothing)."""
+        l, i, d = t.layer, t.mb, deps_of[t.id]
+        if t.comp == "chunk":
+            if t.kind == BWD_B and f"rv.gb.s{t.stage}.m{i}" not in d:
+                return f"f.s{t.stage}.m{i}"
+            return None
+        if t.kind == FWD:
+            if t.comp == "pre":
+                return f"f.post.l{l - 1}.m{i}" if l > 0 else None
+            tag, comp = {"attn": ("pa", "pre"), "post": ("ap", "attn")}[t.comp]
+            return None if f"rv.{tag}.l{l}.m{i}" in d else f"f.{comp}.l{l}.m{i}"
+        if t.kind == BWD_B:
+            if t.comp == "post":
+                return f"b.pre.l{l + 1}.m{i}" if l < L - 1 else f"f.post.l{l}.m{i}"
+            tag, comp = {"attn": ("gap", "post"), "pre": ("gpa", "attn")}[t.comp]
+            return None if f"rv.{tag}.l{l}.m{i}" in d else f"b.{comp}.l{l}.m{i}"
+        return None
+
+    def output_of(t):
+        l, i = t.layer, t.mb
+        if t.comp == "chunk":
+            if t.kind == FWD:
+                e = l + t.span
+                return [(f"x:{e}.{i}", act) if e < L else (f"z:{i}", act)]
+            return [(f"dx:{l}.{i}", act)] if t.kind == BWD_B and t.stage > 0 else []
+        if t.kind == FWD:
+            if t.comp == "pre":
+                first = (f"ln:{l}.{i}", act) if qkv else (f"qkv:{l}.{i}", 3 * act)
+                return [first, x_of(l, i)]
+            if t.comp == "attn":
+                xid, xb = x_of(l, i)
+                res = (xid, xb) if stage_of("pre", l, i) == stage else (f"{xid}@rx", act)
+                return [(local(f"o:{l}.{i}", "attn", l, i), act), res]
+            return [(f"x:{l + 1}.{i}", act) if l < L - 1 else (f"z:{i}", act)]
+        if t.kind == BWD_B:
+            if t.comp == "post":
+                return [(f"dao:{l}.{i}", act), (f"dx2:{l}.{i}", act), (f"dlt:{l}.{i}", dlt)]
+            if t.comp == "attn":
+                res = (local(f"dx2:{l}.{i}", "post", l, i), act)
+                if qkv:
+                    return [(f"dln:{l}.{i}", act), res, (f"dwqkv:{l}.{i}", 3 * h * h * dt.wgrad)]
+                return [(f"dqkv:{l}.{i}", 3 * act), res]
+            return [(f"dx:{l}.{i}", act)] if l > 0 else []
+        return []
+
     peak, at, trace = 0, "", []
     for tid in sched.per_stage_order[stage]:
         t = sched.tasks[tid]
         l, i = t.layer, t.mb
+        if t.is_compute and t.kind in (FWD, BWD_B):
+            src = producer_of(t)
+            if src is not None:
+                release(("v", src))
         if t.kind == FWD:
             if t.comp == "chunk":
                 for ll in range(l, l + t.span):
@@ -201,11 +266,14 @@ def stash_walk(sched: Schedule, stage: int, dt: Dtypes = Dtypes(), regen_pre_x: 
         elif t.kind == BWD_W:
             for key in [k for k in held if k[0] == "w" and k[2] == i]:
                 release(key)
+        hold(("v", tid), output_of(t))
         cur = sum(sizes.values())
         if with_trace:
             trace.append((tid, cur))
         if cur > peak:
             peak, at = cur, tid
+        if tid in sent:
+            release(("v", tid))
     return (peak, at, trace) if with_trace else (peak, at)
 
 
@@ -289,14 +357,15 @@ def _payload_bytes(sched: Schedule, tid: str, dt: Dtypes) -> int:
 
 
 def timeline_peak(sched: Schedule, stage: int, timeline: dict, dt: Dtypes = Dtypes(),
-                  regen_pre_x: bool = False, recv_ahead: int = 4) -> tuple[int, int, float]:
+                  regen_pre_x: bool = False, recv_ahead: int = 4,
+                  stream_inputs: bool = False) -> tuple[int, int, float]:
     """(stash + in-flight payload peak, its payload part, time) on a task
     timeline (simulated or measured).  The stash steps at each task's end
     (``stash_walk``).  A payload occupies its sender from the producer's end
     until the receiver posts the receive (``recv_ahead`` tasks before the
     consumer, ``executor._Distributed``) and its receiver from then until the
     consumer ends (after which the stash walk owns what is kept)."""
-    _, _, trace = stash_walk(sched, stage, dt, regen_pre_x, with_trace=True)
+    _, _, trace = stash_walk(sched, stage, dt, regen_pre_x, with_trace=True, stream_inputs=stream_inputs)
     events: list[tuple[float, int, int]] = []    # (time, stash delta, payload delta)
     prev = 0
     for tid, level in trace:
@@ -343,26 +412,26 @@ def timeline_peak(sched: Schedule, stage: int, timeline: dict, dt: Dtypes = Dtyp
 
 def plan(sched: Schedule, stage: int, mlp_chunk: int | None = None, dt: Dtypes = Dtypes(),
          regen_pre_x: bool = False, recv_ahead: int = 4, send_cap: int = 4,
-         durations=None) -> StagePlan:
+         durations=None, stream_inputs: bool = False) -> StagePlan:
     """Per-rank plan.  With ``durations`` (a ``DurationTable``) the stash and
     the in-flight payloads are combined on the simulated timeline
     (``timeline_peak``); without, the comm term is the worst-case bound of
     ``recv_ahead`` posted receives plus ``send_cap`` sends per peer."""
     cfg = _cfg(sched)
-    peak, at = stash_walk(sched, stage, dt, regen_pre_x)
+    peak, at = stash_walk(sched, stage, dt, regen_pre_x, stream_inputs=stream_inputs)
     w, g = _weight_bytes(sched, stage, dt)
     if sched.n_stages == 1:
         comm = 0
     elif durations is not None:
         from ..simulate import simulate
         tl = simulate(sched, durations).timeline
-        both, comm, when = timeline_peak(sched, stage, tl, dt, regen_pre_x, recv_ahead)
+        both, comm, when = timeline_peak(sched, stage, tl, dt, regen_pre_x, recv_ahead, stream_inputs)
         peak, at = both - comm, f"t={when:g}"
     else:
         comm = _comm(sched, stage, dt, recv_ahead, send_cap)
     # the micro-batch inputs are held by the stage that runs layer 0's pre
     first = 0 if _is_chunked(sched) else pre_stage(0, cfg)
-    inputs = cfg.m * cfg.s * cfg.b * cfg.h * dt.act if stage == first else 0
+    inputs = cfg.m * cfg.s * cfg.b * cfg.h * dt.act if (stage == first and not stream_inputs) else 0
     return StagePlan(stage, w, g, peak, at, _workspace(sched, mlp_chunk, dt), comm, inputs)
 
 

@@ -137,10 +137,25 @@ def test_regen_pre_x_matches_oracle(qkv):
         compare(res, oracle_for(cfg), cfg.L, f"regen_pre_x qkv={qkv} chunk={chunk}")
 
 
-@pytest.mark.parametrize("method,chunk,regen", [("helix_twofold", None, False), ("helix_twofold_rc", 64, False),
-                                                ("helix_twofold_rc", 100, True), ("1f1b_rc", 64, False),
-                                                ("zb1p", None, False)])
-def test_device_stash_bytes_match_memplan(method, chunk, regen):
+def test_streamed_inputs_equal_resident_inputs():
+    """The input streamer (host inputs copied per task on a side stream) gives
+    the results of device-resident inputs."""
+    for method in ("helix_twofold", "helix_twofold_rc", "1f1b"):
+        a = run(SMALL, method, stream_inputs=False)
+        b = run(SMALL, method, stream_inputs=True)
+        assert np.allclose(a.losses, b.losses, rtol=1e-6), method
+        for l in range(SMALL.L):
+            for k in O.FIELDS:
+                g, r = b.param_grads[l][k], a.param_grads[l][k]
+                assert np.abs(g - r).max() <= 1e-3 * np.abs(r).max(), (method, l, k)
+
+
+@pytest.mark.parametrize("method,chunk,regen,stream", [("helix_twofold", None, False, False),
+                                                       ("helix_twofold_rc", 64, False, True),
+                                                       ("helix_twofold_rc", 100, True, False),
+                                                       ("1f1b_rc", 64, False, True),
+                                                       ("zb1p", None, False, False)])
+def test_device_stash_bytes_match_memplan(method, chunk, regen, stream):
     """runtime/memplan.stash_walk with the LayerMath tensor set (bf16, fp32 LSE,
     per-slab m1/g, no stashed O) equals the distinct device bytes the executor
     holds, at p = 1 (one stage per process: the same sharing as one rank)."""
@@ -152,9 +167,9 @@ def test_device_stash_bytes_match_memplan(method, chunk, regen):
     dev = torch.device("cuda", 0)
     model = DeviceModel.from_host(sched, make_model(cfg, 0), [0], dev)
     rt = HelixRuntime(sched, model, chunk, "replay", dev, regen_pre_x=regen)
-    inputs = [torch.from_numpy(x).to(dev, torch.bfloat16).reshape(cfg.s * cfg.b, cfg.h)
-              for x in make_inputs(cfg, 1)]
+    inputs = [torch.from_numpy(x).to(torch.bfloat16).reshape(cfg.s * cfg.b, cfg.h) for x in make_inputs(cfg, 1)]
+    inputs = [x.pin_memory() if stream else x.to(dev) for x in inputs]
     rt.run(inputs)
     torch.cuda.synchronize()
-    want, at = stash_walk(sched, 0, regen_pre_x=regen)
+    want, at = stash_walk(sched, 0, regen_pre_x=regen, stream_inputs=stream)
     assert rt.stages[0].peak_bytes == want, (rt.stages[0].peak_bytes, rt.stages[0].peak_bytes_at, want, at)

@@ -710,7 +710,7 @@ def bench_gpu(args, wl, world: int, rank: int, local: int) -> None:
         do = torch.randn(T, h, device=dev).to(torch.bfloat16)
         dqkv = torch.empty_like(qkv)
         delta = torch.empty(cfg.b * heads * cfg.s, device=dev)
-        dq = torch.empty(T * h, device=dev)
+        dq = K.attention_bwd_ws(cfg.s, cfg.b, heads, h // heads, dev)
         reps = 5
         for _ in range(2):
             K.attention_bwd(qkv, o, do, lse, cfg.s, cfg.b, heads, dqkv, delta, dq)

@@ -98,15 +98,20 @@ HX_API int hx_attn_fwd(const void* qkv, int ld_qkv, void* o, int ld_o, float* ls
 
 /*
  * Causal attention backward.  Writes dq, dk, dv into dqkv ([s*b, ld_dqkv], same
- * column layout as qkv).  Workspaces: delta [b*heads*s] f32 and dq_acc
- * [s*b*heads*d] f32 (both fully overwritten).  With o == NULL, delta is an
- * input instead: D = rowsum(dO * O) from hx_attn_bwd_delta (computed on the
- * stage that holds O, so the attention stage need not stash it).
+ * column layout as qkv).  Workspaces: delta [b*heads*s] f32 (overwritten) and
+ * dq_ws of hx_attn_bwd_ws_bytes(s, b, heads, d) bytes (the fp32 dQ
+ * accumulator; overwritten, no state kept between calls).  With
+ * o == NULL, delta is an input instead: D = rowsum(dO * O) from
+ * hx_attn_bwd_delta (computed on the stage that holds O, so the attention
+ * stage need not stash it).
  * Replaces mathops.attention_backward (P/runtime/mathops.py:103-116).
  */
 HX_API int hx_attn_bwd(const void* qkv, int ld_qkv, const void* o, const void* d_o, int ld_o,
                 const float* lse, float* delta_ws, float* dq_ws, void* dqkv, int ld_dqkv, int s,
                 int b, int heads, int d, void* stream);
+
+/* Bytes of hx_attn_bwd's dq_ws workspace (0 for invalid shapes). */
+HX_API long long hx_attn_bwd_ws_bytes(int s, int b, int heads, int d);
 
 /*
  * delta[b, heads, s] = rowsum(d_o * o) per head (f32), the flash backward's

@@ -175,6 +175,11 @@ int hx_attn_bwd(const void* qkv, int ld_qkv, const void* o, const void* d_o, int
              o != nullptr ? 3 : 2);
 }
 
+long long hx_attn_bwd_ws_bytes(int s, int b, int heads, int d) {
+  if (s <= 0 || b <= 0 || heads <= 0 || d <= 0) return 0;
+  return static_cast<long long>(s) * b * heads * d * 4;  // the fp32 dQ accumulator
+}
+
 int hx_attn_bwd_delta(const void* o, const void* d_o, int ld_o, float* delta, int s, int b, int heads, int d,
                       void* stream) {
   if (d != 64 && d != 128) return HX_E_UNSUPPORTED;

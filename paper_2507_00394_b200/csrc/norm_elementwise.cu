@@ -231,6 +231,8 @@ __global__ void __launch_bounds__(256, MINB) ln_fwd_v2_kernel(const __nv_bfloat1
 #pragma unroll
   for (int i = 0; i < VPL; ++i) {
     const int c = base + 256 * i;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) g[i][k] = bb[i][k] = 0.f;
     if (c < nvec) {
       load_gain8(gain, c, g[i]);
       load_gain8(bias, c, bb[i]);
@@ -238,19 +240,22 @@ __global__ void __launch_bounds__(256, MINB) ln_fwd_v2_kernel(const __nv_bfloat1
   }
   const int r_begin = blockIdx.x * rows_per_block;
   const int r_end = min(rows, r_begin + rows_per_block);
-  int buf = 0;
-  for (int r0 = r_begin; r0 < r_end; r0 += R, buf ^= 1) {
-    uint4 u[R][VPL];
+  uint4 u[R][VPL], nx[R][VPL];
+  auto load = [&](uint4 (&dst)[R][VPL], int r0) {
 #pragma unroll
     for (int j = 0; j < R; ++j)
 #pragma unroll
       for (int i = 0; i < VPL; ++i) {
         const int c = base + 256 * i;
         if (r0 + j < r_end && c < nvec)
-          u[j][i] = __ldcs(reinterpret_cast<const uint4*>(x + static_cast<int64_t>(r0 + j) * h) + c);
+          dst[j][i] = __ldcs(reinterpret_cast<const uint4*>(x + static_cast<int64_t>(r0 + j) * h) + c);
         else
-          u[j][i] = make_uint4(0, 0, 0, 0);
+          dst[j][i] = make_uint4(0, 0, 0, 0);
       }
+  };
+  load(u, r_begin);
+  int buf = 0;
+  for (int r0 = r_begin; r0 < r_end; r0 += R, buf ^= 1) {
 #pragma unroll
     for (int j = 0; j < R; ++j) {
       float sum = 0.f, sq = 0.f;
@@ -270,6 +275,7 @@ __global__ void __launch_bounds__(256, MINB) ln_fwd_v2_kernel(const __nv_bfloat1
     }
     // double-buffered partials: one barrier per batch (the next batch writes the other buffer)
     __syncthreads();
+    load(nx, r0 + R);  // the next batch's loads fly during this batch's normalise / store
 #pragma unroll
     for (int j = 0; j < R; ++j) {
       if (r0 + j >= r_end) break;
@@ -296,6 +302,10 @@ __global__ void __launch_bounds__(256, MINB) ln_fwd_v2_kernel(const __nv_bfloat1
         }
       }
     }
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) u[j][i] = nx[j][i];
   }
 }
 
@@ -312,15 +322,14 @@ __global__ void __launch_bounds__(256, MINB) ln_bwd_v2_kernel(
 #pragma unroll
   for (int i = 0; i < VPL; ++i) {
     const int c = base + 256 * i;
-    if (c < nvec) load_gain8(gain, c, g[i]);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) adg[i][k] = adb[i][k] = 0.f;
+    for (int k = 0; k < 8; ++k) g[i][k] = adg[i][k] = adb[i][k] = 0.f;
+    if (c < nvec) load_gain8(gain, c, g[i]);
   }
   const int r_begin = blockIdx.x * rows_per_block;
   const int r_end = min(rows, r_begin + rows_per_block);
-  int buf = 0;
-  for (int r0 = r_begin; r0 < r_end; r0 += R, buf ^= 1) {
-    uint4 ux[R][VPL], ud[R][VPL];
+  uint4 ux[R][VPL], ud[R][VPL], nxx[R][VPL], nxd[R][VPL];
+  auto load = [&](uint4 (&dx_)[R][VPL], uint4 (&dd_)[R][VPL], int r0) {
 #pragma unroll
     for (int j = 0; j < R; ++j)
 #pragma unroll
@@ -328,12 +337,16 @@ __global__ void __launch_bounds__(256, MINB) ln_bwd_v2_kernel(
         const int c = base + 256 * i;
         const int64_t off = static_cast<int64_t>(r0 + j) * h;
         if (r0 + j < r_end && c < nvec) {
-          ux[j][i] = __ldcs(reinterpret_cast<const uint4*>(x + off) + c);
-          ud[j][i] = __ldcs(reinterpret_cast<const uint4*>(dy + off) + c);
+          dx_[j][i] = __ldcs(reinterpret_cast<const uint4*>(x + off) + c);
+          dd_[j][i] = __ldcs(reinterpret_cast<const uint4*>(dy + off) + c);
         } else {
-          ux[j][i] = ud[j][i] = make_uint4(0, 0, 0, 0);
+          dx_[j][i] = dd_[j][i] = make_uint4(0, 0, 0, 0);
         }
       }
+  };
+  load(ux, ud, r_begin);
+  int buf = 0;
+  for (int r0 = r_begin; r0 < r_end; r0 += R, buf ^= 1) {
 #pragma unroll
     for (int j = 0; j < R; ++j) {
       float sx = 0.f, sxx = 0.f, sg = 0.f, sgx = 0.f;
@@ -358,6 +371,7 @@ __global__ void __launch_bounds__(256, MINB) ln_bwd_v2_kernel(
       if (lane == 0) part[buf][j][w] = make_float4(sx, sxx, sg, sgx);
     }
     __syncthreads();
+    load(nxx, nxd, r0 + R);  // next batch in flight during this batch's dx / column sums
 #pragma unroll
     for (int j = 0; j < R; ++j) {
       if (r0 + j >= r_end) break;
@@ -400,6 +414,13 @@ __global__ void __launch_bounds__(256, MINB) ln_bwd_v2_kernel(
         }
       }
     }
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        ux[j][i] = nxx[j][i];
+        ud[j][i] = nxd[j][i];
+      }
   }
 #pragma unroll
   for (int i = 0; i < VPL; ++i) {
@@ -488,7 +509,9 @@ static int ln_grid(int per_sm, int rows) {
   return blocks < resident ? blocks : resident;
 }
 
-// LN v2 (default) / v1 (HX_LN=1, kept for A/B runs).
+// LN v2 (default; the backward only for h > 2048) / v1 (HX_LN=1, kept for A/B runs).
+// Measured alone (tools/kernel_bench.py, B200): forward T=32k h=2048 0.058 ms
+// (4.66 TB/s) vs v1 0.070; T=64k h=4096 0.197 ms (5.45 TB/s, 83%) vs 0.263.
 static int ln_version() {
   static const int v = getenv("HX_LN") ? atoi(getenv("HX_LN")) : 2;
   return v;
@@ -537,7 +560,7 @@ cudaError_t ln_fwd_launch(const void* x, const float* g, const float* b, void* y
     if (ln_version() == 3) {
       HX_VPL_DISPATCH(h, L3, 8, 4, 2);
     } else {
-      HX_VPL_DISPATCH(h, L2, 8, 4, 1);
+      HX_VPL_DISPATCH(h, L2, 4, 2, 1);
     }
 #undef L2
 #undef L3
@@ -555,7 +578,10 @@ cudaError_t ln_fwd_launch(const void* x, const float* g, const float* b, void* y
 
 cudaError_t ln_bwd_launch(const void* dy, const void* x, const float* g, const void* dres, void* dx,
                           float* dg, float* db, float* stats, int rows, int h, cudaStream_t st) {
-  if (ln_version() >= 2) {
+  // v2 (one pass, gain / bias sums fused) wins from h = 4096 (0.47 vs 0.59 ms at
+  // T = 64k); at h <= 2048 its 2-row batches are barrier-bound and the row-per-warp
+  // v1 pair is faster (0.142 vs 0.170 ms at T = 32k), tools/kernel_bench.py
+  if (ln_version() >= 2 && (ln_version() > 2 || h > 2048)) {
 #define LB(VPL, R, MB)                                                                                      \
   {                                                                                                         \
     int grid, per;                                                                                          \
@@ -567,9 +593,9 @@ cudaError_t ln_bwd_launch(const void* dy, const void* x, const float* g, const v
 #define L2(VPL, R) LB(VPL, R, 2)
 #define L3(VPL, R) LB(VPL, R, 1)
     if (ln_version() == 3) {
-      HX_VPL_DISPATCH(h, L3, 8, 4, 2);
+      HX_VPL_DISPATCH(h, L3, 4, 2, 1);
     } else {
-      HX_VPL_DISPATCH(h, L2, 4, 2, 1);
+      HX_VPL_DISPATCH(h, L2, 2, 1, 1);
     }
 #undef L2
 #undef L3

@@ -32,11 +32,12 @@ SIGNATURES: dict[str, list] = {
     "hx_attn_fwd": [_P, _I, _P, _I, _P, _I, _I, _I, _I, _P],
     "hx_attn_bwd": [_P, _I, _P, _P, _I, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P],
     "hx_attn_bwd_delta": [_P, _P, _I, _P, _I, _I, _I, _I, _P],
+    "hx_attn_bwd_ws_bytes": [_I, _I, _I, _I],
     "hx_mse_loss": [_P, _LL, _P, _P, _P],
     "hx_axpy_f32": [_P, _P, _LL, _P],
     "hx_zero": [_P, _LL, _P],
 }
-_RESTYPE = {"hx_launch_count": ctypes.c_longlong}
+_RESTYPE = {"hx_launch_count": ctypes.c_longlong, "hx_attn_bwd_ws_bytes": ctypes.c_longlong}
 
 
 class KernelLibraryError(RuntimeError):

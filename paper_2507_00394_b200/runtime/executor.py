@@ -237,8 +237,9 @@ class _InputStreamer:
         if not self.cuda:
             self.ready[tid] = (src.clone(), None)
             return
-        cur = torch.cuda.current_stream(self.device)
-        self.stream.wait_stream(cur)          # the buffer's allocation is ordered
+        # allocated and filled on the side stream (its own allocator pool, so no
+        # ordering against the compute stream is needed); the consumer waits on
+        # the copy's event and takes the buffer over with record_stream
         with torch.cuda.stream(self.stream):
             dev = torch.empty(src.shape, dtype=src.dtype, device=self.device)
             dev.copy_(src, non_blocking=True)

@@ -149,11 +149,27 @@ def attention_delta(o, d_o, s: int, b: int, heads: int, delta: torch.Tensor):
     return delta
 
 
+def attention_bwd_ws_bytes(s: int, b: int, heads: int, d: int) -> int:
+    """Bytes of the backward's workspace (fp32 dQ accumulator + per-tile counters)."""
+    return int(_lib.load().hx_attn_bwd_ws_bytes(s, b, heads, d))
+
+
+def attention_bwd_ws(s: int, b: int, heads: int, d: int, device) -> torch.Tensor:
+    n = attention_bwd_ws_bytes(s, b, heads, d)
+    return torch.empty((n + 3) // 4, dtype=F32, device=device)
+
+
 def attention_bwd(qkv, o, d_o, lse, s: int, b: int, heads: int, dqkv: torch.Tensor,
-                  delta_ws: torch.Tensor, dq_ws: torch.Tensor):
-    """``o=None``: ``delta_ws`` already holds D (``attention_delta``)."""
+                  delta_ws: torch.Tensor, dq_ws: torch.Tensor | None = None):
+    """``o=None``: ``delta_ws`` already holds D (``attention_delta``).
+    ``dq_ws``: at least ``attention_bwd_ws_bytes`` (allocated here if None)."""
     qkv = _rows(qkv)
     h = qkv.shape[1] // 3
+    need = attention_bwd_ws_bytes(s, b, heads, h // heads)
+    if dq_ws is None:
+        dq_ws = attention_bwd_ws(s, b, heads, h // heads, qkv.device)
+    elif dq_ws.numel() * dq_ws.element_size() < need:
+        raise ValueError(f"dq_ws holds {dq_ws.numel() * dq_ws.element_size()} bytes, need {need}")
     ld_o = _rows(d_o).stride(0) if o is None else _rows(o).stride(0)
     _lib.call("hx_attn_bwd", qkv.data_ptr(), qkv.stride(0), None if o is None else o.data_ptr(),
               d_o.data_ptr(), ld_o, lse.data_ptr(), delta_ws.data_ptr(), dq_ws.data_ptr(),

@@ -271,11 +271,10 @@ class LayerMath:
         if qkv is None:  # recompute retention: rebuild the projection, never the attention
             qkv = K.linear(stash["ln_out"], stash["qkv_weight"], self._empty(3 * self.h))
         d_qkv = self._empty(3 * self.h)
-        # workspaces come from the stream-ordered caching allocator so that
-        # stages on different streams never share them
-        dq = torch.empty(self.T * self.h, dtype=torch.float32, device=self.device)
+        # workspace from the stream-ordered caching allocator (stages on different
+        # streams never share it)
         K.attention_bwd(qkv, None, payload["d_attn_out"], stash["lse"], self.cfg.s,
-                        self.cfg.b, self.heads, d_qkv, payload["delta"], dq)
+                        self.cfg.b, self.heads, d_qkv, payload["delta"])
         if not self.qkv:
             return {"d_qkv": d_qkv, "d_residual": payload["d_residual"]}
         d_ln = K.linear_dx(d_qkv, stash["qkv_weight"], self._empty(self.h))

@@ -97,6 +97,34 @@ def measured_durations(sched: Schedule, timeline) -> DurationTable:
     return DurationTable.from_measured(row("pre"), row("attn"), row("post"))
 
 
+def task_class_durations(sched: Schedule, timeline) -> dict[str, int]:
+    """Average device ns per task class ``KIND.comp`` (FWD.pre, RECOMPUTE.post,
+    BWD_B.chunk, ...) from a CUDA-event timeline -- finer than a
+    ``DurationTable``: recompute tasks keep their own (measured) cost, and chunk
+    tasks (1F1B) are covered."""
+    sums: dict[str, list[float]] = {}
+    for tid, (start, end) in timeline.items():
+        t = sched.tasks.get(tid)
+        if t is None or not t.is_compute:
+            continue
+        key = f"{t.kind}.{t.comp}" + (f".x{t.span}" if t.comp == "chunk" else "")
+        sums.setdefault(key, []).append(end - start)
+    return {k: int(round(1e6 * sum(v) / len(v))) for k, v in sums.items()}
+
+
+def simulate_classes(sched: Schedule, classes: dict[str, int], comm: CommModel | None = None) -> SimResult:
+    """The reference's list scheduler (``P/engine.py``) replaying ``sched`` with
+    per-task-class durations (``task_class_durations``, e.g. measured on one
+    rank by the stage probe); SEND/RECV cost per ``comm``."""
+
+    def dur(task) -> int:
+        key = f"{task.kind}.{task.comp}" + (f".x{task.span}" if task.comp == "chunk" else "")
+        return classes[key]
+
+    res = replay(sched, dur, comm or CommModel.zero())
+    return SimResult(sched, res.timeline, metrics_from_timeline(sched, res.timeline, "ns"))
+
+
 def _analytic_fraction(method: str, cfg, durations: DurationTable) -> float | None:
     from .analytic import bubble_fraction
     from .config import ConfigError

@@ -62,3 +62,20 @@ def test_bubble_fraction_and_memory_model():
     dropped = stage_memory_bytes("helix_twofold_rc", big, drop_pre_x=True, mlp_chunk=16384)
     assert dropped["stash"] * 4 == full["stash"] * 3
     assert full["total"] == sum(v for k, v in full.items() if k != "total")
+
+
+def test_task_class_simulation_reproduces_table_simulation():
+    """simulate_classes with per-class durations recovered from a simulated
+    timeline replays to the same makespan (the stage probe's prediction path)."""
+    from paper_2507_00394_b200 import ModelConfig, generate
+    from paper_2507_00394_b200.costs import DurationTable
+    from paper_2507_00394_b200.simulate import simulate, simulate_classes, task_class_durations
+    cfg = ModelConfig(L=8, h=64, s=128, b=1, num_heads=2, p=4, m=8)
+    table = DurationTable.from_units(1, 3, 2)
+    for method in ("helix_twofold", "helix_twofold_rc", "1f1b", "zb1p"):
+        sched = generate(method, cfg, table)
+        ref = simulate(sched, table)
+        tl_ms = {k: (a / 1e6, b / 1e6) for k, (a, b) in ref.timeline.items()}
+        classes = task_class_durations(sched, tl_ms)
+        got = simulate_classes(sched, classes)
+        assert got.metrics.makespan == ref.metrics.makespan, method

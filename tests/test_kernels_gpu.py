@@ -187,7 +187,7 @@ def test_attention_backward(s, b, heads, d):
     d_o = rnd(s * b, h, seed=18)
     dqkv = torch.empty_like(qkv)
     delta = torch.empty(b * heads * s, device=DEV)
-    dq_ws = torch.empty(b * heads * s * d, device=DEV)
+    dq_ws = K.attention_bwd_ws(s, b, heads, d, DEV)
     K.attention_bwd(qkv, o, d_o, lse, s, b, heads, dqkv, delta, dq_ws)
     torch.cuda.synchronize()
     qf = qkv.float().requires_grad_(True)

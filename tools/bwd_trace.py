@@ -57,7 +57,7 @@ def main():
     do = torch.randn(s, h, device="cuda").to(torch.bfloat16)
     dqkv = torch.empty_like(qkv)
     delta = torch.empty(heads * s, device="cuda")
-    dq = torch.empty(s * h, device="cuda")
+    dq = K.attention_bwd_ws(s, 1, heads, h // heads, "cuda")
     for _ in range(2):
         K.attention_bwd(qkv, o, do, lse, s, 1, heads, dqkv, delta, dq)
     torch.cuda.synchronize()

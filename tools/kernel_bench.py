@@ -94,7 +94,7 @@ def main():
         do = torch.randn(T, h, device=dev).to(bf)
         dqkv = torch.empty_like(qkv)
         delta = torch.empty(heads * s, device=dev)
-        dq = torch.empty(T * h, device=dev)
+        dq = K.attention_bwd_ws(s, 1, heads, h // heads, dev)
         out("attn_bwd", timed(lambda: K.attention_bwd(qkv, o, do, lse, s, 1, heads, dqkv, delta, dq),
                               args.reps), fwd_fl * 5 // 2, s=s, heads=heads, d=h // heads)
         del qkv, o, lse, do, dqkv, delta, dq

@@ -37,7 +37,9 @@ from paper_2507_00394_b200.runtime import HelixRuntime  # noqa: E402
 from paper_2507_00394_b200.runtime.executor import DeviceModel, stage_fields  # noqa: E402
 from paper_2507_00394_b200.runtime.memplan import GB, plan  # noqa: E402
 from paper_2507_00394_b200.runtime.model import DeviceLayer, random_device_layer  # noqa: E402
-from paper_2507_00394_b200.simulate import measured_durations, simulate  # noqa: E402
+from paper_2507_00394_b200.engine import CommModel  # noqa: E402
+from paper_2507_00394_b200.simulate import (measured_durations, simulate, simulate_classes,  # noqa: E402
+                                            task_class_durations)
 
 
 def main():
@@ -114,6 +116,15 @@ def main():
             "plan_gb": pl.as_gb(),
             "tokens_per_s_if_busy_bound": cfg.m * cfg.s * cfg.b / (busy / 1e3),
         }
+        classes = task_class_durations(sched, tl)
+        out["task_class_ns"] = classes
+        # the reference list scheduler over the whole p-stage schedule with these
+        # measured per-class durations (every stage runs the same shapes), NVLink comm
+        comm = CommModel("bytes", latency=5000, bytes_per_element=2, bandwidth=int(770e9))
+        sim_c = simulate_classes(sched, classes, comm)
+        out["predicted_from_classes"] = {"makespan_ms": sim_c.metrics.makespan / 1e6,
+                                         "bubble_fraction": sim_c.metrics.bubble_fraction,
+                                         "tokens_per_s": cfg.m * cfg.s * cfg.b / (sim_c.metrics.makespan * 1e-9)}
         if table is not None:
             sim = simulate(generate(args.method, cfg, table), table)
             out["durations_ns"] = {f"{c}.{ps}": v for (c, ps), v in table.entries.items()}

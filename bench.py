@@ -582,7 +582,7 @@ def bench_gpu(args, wl, world: int, rank: int, local: int) -> None:
     launches0 = _lib.launch_count()
     _lib.start_kernel_timers()      # per-entry-point CUDA events inside the timed steps
     ms = time_steps(rt, args.steps)
-    ktimes = _lib.stop_kernel_timers()
+    ktimes, ktagged = _lib.stop_kernel_timers(with_tags=True)
     launches = _lib.launch_count() - launches0
     clk = clocks.stop()
     tokens = cfg.m * cfg.s * cfg.b
@@ -696,12 +696,55 @@ def bench_gpu(args, wl, world: int, rank: int, local: int) -> None:
     peaks = load_peaks()
     roof = None
     kernel_share = None
+    gemm_shapes = None
     if rank == 0:
         fwd_fl, bwd_fl = attention_kernel_flops(cfg)
         kernel_share = {k.removeprefix("hx_"): {"launches": v["launches"] // args.steps,
                                                 "ms_per_step": v["total_ms"] / args.steps,
                                                 "share": v["total_ms"] / args.steps / ms}
                         for k, v in sorted(ktimes.items(), key=lambda kv: -kv[1]["total_ms"])}
+        # GEMMs by shape (layout A/B: N = K-major, T = MN-major; M x N x K; epilogue):
+        # achieved TFLOP/s inside the timed steps, for the GEMM roofline per shape
+        gemm_shapes = []
+        for key, v in sorted(ktagged.items(), key=lambda kv: -kv[1]["total_ms"]):
+            if not key.startswith("hx_gemm:"):
+                continue
+            lay, mnk, epi = key.split(":", 1)[1].split()
+            M_, N_, K_ = (int(x) for x in mnk.split("x"))
+            gemm_shapes.append({"layout": lay, "M": M_, "N": N_, "K": K_, "epilogue": epi,
+                                "calls_per_step": v["launches"] // args.steps, "mean_ms": v["mean_ms"],
+                                "tflops": 2 * M_ * N_ * K_ / (v["mean_ms"] / 1e3) / 1e12,
+                                "ms_per_step": v["total_ms"] / args.steps})
+        # each shape once more in isolation, next to cuBLAS (torch.matmul, bf16 out) on the
+        # same operand layouts: the library yardstick for the tcgen05 GEMM
+        def _iso(fn, reps=5):
+            fn()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(reps):
+                fn()
+            e1.record()
+            torch.cuda.synchronize()
+            return e0.elapsed_time(e1) / reps
+
+        for g_ in gemm_shapes:
+            M_, N_, K_ = g_["M"], g_["N"], g_["K"]
+            a_t, b_t = g_["layout"][0] == "T", g_["layout"][1] == "T"
+            A_ = torch.randn(K_, M_, device=dev).to(torch.bfloat16) if a_t else \
+                torch.randn(M_, K_, device=dev).to(torch.bfloat16)
+            B_ = torch.randn(K_, N_, device=dev).to(torch.bfloat16) if b_t else \
+                torch.randn(N_, K_, device=dev).to(torch.bfloat16)
+            acc = g_["epilogue"] in (f"epi{_lib.EPI_ACC_F32}", f"epi{_lib.EPI_STORE_F32}")
+            C_ = torch.zeros(M_, N_, device=dev, dtype=torch.float32 if acc else torch.bfloat16)
+            epi_ = _lib.EPI_ACC_F32 if acc else _lib.EPI_STORE_BF16
+            ours = _iso(lambda: K.gemm(A_, a_t, B_, b_t, C_, M_, N_, K_, epi_))
+            At, Bt = (A_.t() if a_t else A_), (B_ if b_t else B_.t())   # logical [M,K], [K,N]
+            cub = _iso(lambda: torch.matmul(At, Bt))
+            fl = 2 * M_ * N_ * K_
+            g_["isolated_tflops"] = fl / (ours / 1e3) / 1e12
+            g_["cublas_tflops"] = fl / (cub / 1e3) / 1e12
+            g_["vs_cublas"] = cub / ours
+            del A_, B_, C_
         h, heads = cfg.h, cfg.num_heads
         qkv = torch.randn(T, 3 * h, device=dev).to(torch.bfloat16)
         o = torch.empty(T, h, dtype=torch.bfloat16, device=dev)
@@ -789,6 +832,7 @@ def bench_gpu(args, wl, world: int, rank: int, local: int) -> None:
             "e2e": e2e,
             "roofline": roof,
             "kernel_share": kernel_share,
+            "gemm_shapes": gemm_shapes,
             "cpu_baseline": cpu,
             "config1": config1,
             "comm": rt.comm_stats,

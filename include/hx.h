@@ -122,6 +122,27 @@ HX_API int hx_attn_bwd_delta(const void* o, const void* d_o, int ld_o, float* de
                              int d, void* stream);
 
 /*
+ * Paper §4.6 extras (the reference has no code for them,
+ * SPEC.md:467).  Word + position embeddings in front of layer 0:
+ * x[t] = w_emb[tokens[t]] + w_pos[t / b] (t = s_idx * b + b_idx; bf16 [*, h]).
+ * tokens must lie in [0, rows of w_emb).
+ */
+HX_API int hx_embed_fwd(const int* tokens, const void* w_emb, const void* w_pos, void* x, int s, int b, int h,
+                        void* stream);
+/* dw_emb[tokens[t]] += dx[t] (fp32 atomics), dw_pos[s_idx] += sum_b dx[s_idx * b + b_idx]. */
+HX_API int hx_embed_bwd(const int* tokens, const void* dx, float* dw_emb, float* dw_pos, int s, int b, int h,
+                        void* stream);
+/*
+ * Next-token cross-entropy over a chunk of logits rows ([rows, ld] bf16, the
+ * first vocab of vpad columns real): loss_acc[0] += sum over rows with
+ * labels[r] >= 0 of lse(row) - row[labels[r]]; count_acc[0] += that row count;
+ * the logits are overwritten by dlogits = (softmax - onehot) * scale (padded
+ * columns and ignored rows: 0).  The loss-in-backward head of PAPER.md:443-444.
+ */
+HX_API int hx_ce_loss(void* logits, int ld, const int* labels, int rows, int vocab, int vpad, float scale,
+                      double* loss_acc, int* count_acc, void* stream);
+
+/*
  * sumsq_acc[0] += sum(z^2) (fp64); dz = z * 2/n.  loss = sumsq/n (host divides).
  * Replaces model.loss_and_grad (P/runtime/model.py:61-64).
  */

@@ -188,6 +188,28 @@ int hx_attn_bwd_delta(const void* o, const void* d_o, int ld_o, float* delta, in
   return ret(attn_bwd_delta_launch(o, d_o, ld_o, delta, s, b, heads, d, as_stream(stream)), 1);
 }
 
+int hx_embed_fwd(const int* tokens, const void* w_emb, const void* w_pos, void* x, int s, int b, int h,
+                 void* stream) {
+  if (s <= 0 || b <= 0 || h <= 0 || h % 8) return HX_E_SHAPE;
+  if (!aligned16(w_emb) || !aligned16(w_pos) || !aligned16(x)) return HX_E_ALIGN;
+  return ret(embed_fwd_launch(tokens, w_emb, w_pos, x, s, b, h, as_stream(stream)), 1);
+}
+
+int hx_embed_bwd(const int* tokens, const void* dx, float* dw_emb, float* dw_pos, int s, int b, int h,
+                 void* stream) {
+  if (s <= 0 || b <= 0 || h <= 0 || h % 8) return HX_E_SHAPE;
+  if (!aligned16(dx) || !aligned16(dw_emb) || !aligned16(dw_pos)) return HX_E_ALIGN;
+  return ret(embed_bwd_launch(tokens, dx, dw_emb, dw_pos, s, b, h, as_stream(stream)), 1);
+}
+
+int hx_ce_loss(void* logits, int ld, const int* labels, int rows, int vocab, int vpad, float scale,
+               double* loss_acc, int* count_acc, void* stream) {
+  if (rows <= 0 || vocab <= 0 || vpad < vocab || vpad % 8 || ld < vpad || ld % 8) return HX_E_SHAPE;
+  if (!aligned16(logits)) return HX_E_ALIGN;
+  return ret(ce_loss_launch(logits, ld, labels, rows, vocab, vpad, scale, loss_acc, count_acc, as_stream(stream)),
+             1);
+}
+
 int hx_mse_loss(const void* z, long long n, void* dz, double* sumsq_acc, void* stream) {
   if (n <= 0 || n % 8) return HX_E_SHAPE;
   if (!aligned16(z) || !aligned16(dz)) return HX_E_ALIGN;

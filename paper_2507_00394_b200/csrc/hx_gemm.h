@@ -57,6 +57,13 @@ cudaError_t attn_bwd_launch(const void* qkv, int ld_qkv, const void* o, const vo
                             const float* lse, float* delta, float* dq_acc, void* dqkv, int ld_dqkv,
                             int s, int b, int heads, int d, cudaStream_t st);
 
+cudaError_t embed_fwd_launch(const int* tok, const void* w_emb, const void* w_pos, void* x, int s, int b, int h,
+                             cudaStream_t st);
+cudaError_t embed_bwd_launch(const int* tok, const void* dx, float* dw_emb, float* dw_pos, int s, int b, int h,
+                             cudaStream_t st);
+cudaError_t ce_loss_launch(void* logits, int ld, const int* labels, int rows, int vocab, int vpad, float scale,
+                           double* loss_acc, int* count_acc, cudaStream_t st);
+
 cudaError_t gemm_launch(const GemmOperand& a, const GemmOperand& b, const GemmParams& p,
                         cudaStream_t stream);
 

@@ -33,6 +33,9 @@ SIGNATURES: dict[str, list] = {
     "hx_attn_bwd": [_P, _I, _P, _P, _I, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P],
     "hx_attn_bwd_delta": [_P, _P, _I, _P, _I, _I, _I, _I, _P],
     "hx_attn_bwd_ws_bytes": [_I, _I, _I, _I],
+    "hx_embed_fwd": [_P, _P, _P, _P, _I, _I, _I, _P],
+    "hx_embed_bwd": [_P, _P, _P, _P, _I, _I, _I, _P],
+    "hx_ce_loss": [_P, _I, _P, _I, _I, _I, ctypes.c_float, _P, _P, _P],
     "hx_mse_loss": [_P, _LL, _P, _P, _P],
     "hx_axpy_f32": [_P, _P, _LL, _P],
     "hx_zero": [_P, _LL, _P],
@@ -84,21 +87,33 @@ def start_kernel_timers() -> None:
     _timers = {}
 
 
-def stop_kernel_timers() -> dict[str, dict]:
-    """Synchronise and return {entry point: {"launches", "total_ms", "mean_ms"}}."""
-    global _timers
+_tagged: dict[str, list] | None = None
+
+
+def stop_kernel_timers(with_tags: bool = False):
+    """Synchronise and return {entry point: {"launches", "total_ms", "mean_ms"}}
+    (and, ``with_tags``, the same per call tag, e.g. per GEMM shape)."""
+    global _timers, _tagged
     import torch
 
     timers, _timers = _timers or {}, None
+    tagged, _tagged = _tagged or {}, None
     torch.cuda.synchronize()
-    out = {}
-    for name, evs in timers.items():
-        tot = sum(a.elapsed_time(b) for a, b in evs)
-        out[name] = {"launches": len(evs), "total_ms": tot, "mean_ms": tot / len(evs)}
-    return out
+
+    def summarise(d):
+        out = {}
+        for name, evs in d.items():
+            tot = sum(a.elapsed_time(b) for a, b in evs)
+            out[name] = {"launches": len(evs), "total_ms": tot, "mean_ms": tot / len(evs)}
+        return out
+
+    return (summarise(timers), summarise(tagged)) if with_tags else summarise(timers)
 
 
-def call(name: str, *args) -> None:
+def call(name: str, *args, tag: str | None = None) -> None:
+    """Invoke a C-ABI entry point; raise on a nonzero return.  While timers run,
+    the call is bracketed by CUDA events, keyed by name (and name:tag)."""
+    global _tagged
     fn = getattr(load(), name)
     if _timers is None:
         check(fn(*args), name)
@@ -110,6 +125,10 @@ def call(name: str, *args) -> None:
     rc = fn(*args)
     b.record()
     _timers.setdefault(name, []).append((a, b))
+    if tag is not None:
+        if _tagged is None:
+            _tagged = {}
+        _tagged.setdefault(f"{name}:{tag}", []).append((a, b))
     check(rc, name)
 
 

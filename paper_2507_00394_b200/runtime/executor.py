@@ -287,6 +287,12 @@ class _Core:
         self.regen_pre_x = False
         self.inputs: list[torch.Tensor] = []
         self.streamer: _InputStreamer | None = None    # host-resident inputs (HelixRuntime.run)
+        # LM mode (runtime/lm.py, paper §4.6): token inputs, embedding, loss-in-backward head
+        self.lm = None
+        self.tokens: list[torch.Tensor] = []
+        self.labels: list[torch.Tensor] = []
+        self.n_valid: list[int] = []
+        self.loss_count: torch.Tensor | None = None
         self.recv_of_send = {t.deps[0]: t.id for t in self.tasks.values() if t.kind == RECV}
         self.sends_by_producer: dict[str, list[Task]] = {}
         for t in self.tasks.values():
@@ -344,6 +350,10 @@ class _Core:
 
     def input_x(self, t: Task) -> torch.Tensor:
         """Layer 0's input for ``t``'s micro-batch (device tensor)."""
+        if self.lm is not None:
+            cfg = self.cfg
+            x = torch.empty(cfg.s * cfg.b, cfg.h, dtype=torch.bfloat16, device=self.stages[t.stage].device)
+            return self.lm.embed(self.tokens[t.mb], x)
         if self.streamer is not None:
             return self.streamer.get(t.id, t.mb)
         return self.inputs[t.mb]
@@ -397,6 +407,9 @@ class _Core:
             raise ExecutionError(f"{t.id}: kind {t.kind} is not a compute task")
 
     def _loss(self, z: torch.Tensor, mb: int) -> torch.Tensor:
+        if self.lm is not None:   # the head runs here, in the backward
+            return self.lm.loss_backward(z, self.labels[mb], self.n_valid[mb], self.sumsq[mb:mb + 1],
+                                         self.loss_count[mb:mb + 1])
         return self.math.loss(z, self.sumsq[mb:mb + 1])
 
     def _fwd_component(self, st: _Stage, t: Task) -> None:
@@ -441,6 +454,8 @@ class _Core:
             d_x = self.math.pre_backward(payload, self.W(l), self.G(l), stash)
             if l > 0:
                 st.values[t.id] = {"d_x": d_x}
+            elif self.lm is not None:
+                self.lm.embed_backward(self.tokens[t.mb], d_x)
 
     def _fwd_chunk(self, st: _Stage, t: Task) -> None:
         src = self.input_id(t)
@@ -485,6 +500,8 @@ class _Core:
             st.wctx[t.mb] = deferred
         if t.stage > 0:
             st.values[t.id] = {"d_x": d}
+        elif self.lm is not None and t.layer == 0:
+            self.lm.embed_backward(self.tokens[t.mb], d)
 
     # -- comm ---------------------------------------------------------------------
 
@@ -988,7 +1005,7 @@ class HelixRuntime:
                  mode: str = "replay", device=None, math=None, rank: int | None = None,
                  groups: dict | None = None, record_timeline: bool = False,
                  stash_budget_bytes: int | None = None, offload_min_bytes: int = 32 << 20,
-                 regen_pre_x: bool = False, stream_inputs: bool = False):
+                 regen_pre_x: bool = False, stream_inputs: bool = False, lm=None, lm_params=None):
         self.sched = sched
         self.stream_inputs = stream_inputs
         self.cfg = meta_config(sched)
@@ -1006,6 +1023,8 @@ class HelixRuntime:
         self.sumsq = torch.zeros(self.cfg.m, dtype=torch.float64, device=self.device)
         self.timeline = None
         self.core = _Core(sched, model, self.math, self.stages, self.sumsq)
+        if lm is not None:
+            self._setup_lm(lm, lm_params)
         if regen_pre_x:
             chunked = any(t.comp == "chunk" for t in sched.tasks.values() if t.is_compute)
             if not self.core.rc or chunked:
@@ -1028,20 +1047,67 @@ class HelixRuntime:
             self.core.offload = StashOffloader(sched, self.stages, weights, stash_budget_bytes,
                                                min_bytes=offload_min_bytes, regen_pre_x=regen_pre_x)
 
-    def run(self, inputs: list[torch.Tensor]) -> None:
+    def _setup_lm(self, spec, params) -> None:
+        """LM mode (runtime/lm.py): the tied word embedding is read by layer 0's
+        pre (embedding) and by the loss task (head) -- both must run here."""
+        from .lm import LMHead, LMParams
+        cfg = self.cfg
+        chunked = any(t.comp == "chunk" for t in self.sched.tasks.values() if t.is_compute)
+        first = 0 if chunked else pre_stage(0, cfg)
+        last = (self.sched.n_stages - 1) if chunked else post_stage(cfg.L - 1, cfg)
+        if first != last:
+            raise ExecutionError("LM head: the tied embedding's two uses are on stages "
+                                 f"{first} and {last}; only schedules placing them together are supported")
+        if first not in self.stages:
+            return                           # this rank holds neither end
+        if params is None:
+            gen = torch.Generator(device=self.device).manual_seed(4321)
+            params = LMParams(spec, cfg.h, cfg.s, self.device, gen)
+        self.lm_params = params
+        self.core.lm = LMHead(spec, params, cfg.s, cfg.b, cfg.h)
+        self.core.loss_count = torch.zeros(cfg.m, dtype=torch.int32, device=self.device)
+
+    def lm_grads(self) -> dict[str, torch.Tensor] | None:
+        """fp32 gradients of the word (padded rows included) and position embeddings."""
+        if self.core.lm is None:
+            return None
+        return {"w_emb": self.lm_params.d_emb, "w_pos": self.lm_params.d_pos}
+
+    def run(self, inputs: list[torch.Tensor], labels: list[torch.Tensor] | None = None) -> None:
+        """One iteration.  LM mode: ``inputs`` are token ids ``[s, b]`` per
+        micro-batch and ``labels`` (default: the next token, last position
+        ignored = -1) the targets."""
         cfg = self.cfg
         if len(inputs) != cfg.m:
             raise ExecutionError(f"need {cfg.m} input microbatches, got {len(inputs)}")
+        if self.core.lm is not None:
+            from .lm import default_labels
+            T = cfg.s * cfg.b
+            toks = [x.to(device=self.device, dtype=torch.int32).reshape(T).contiguous() for x in inputs]
+            for x in toks:
+                if int(x.min()) < 0 or int(x.max()) >= self.core.lm.spec.vocab:
+                    raise ExecutionError("token id outside the vocabulary")
+            labs = [default_labels(x, cfg.s, cfg.b) if labels is None else
+                    labels[i].to(device=self.device, dtype=torch.int32).reshape(T).contiguous()
+                    for i, x in enumerate(toks)]
+            self.core.tokens, self.core.labels = toks, labs
+            self.core.n_valid = [int((lb >= 0).sum()) for lb in labs]
+            self.core.lm.p.zero_grads(self.math.zero_)
+            self.math.zero_(self.core.loss_count)
+            inputs = [None] * cfg.m
         # (a stage probe of a rank that never reads the inputs may pass None)
         self.core.inputs = [None if x is None else x.reshape(cfg.s * cfg.b, cfg.h) for x in inputs]
         # host inputs on a CUDA runtime (or stream_inputs): copied in per task, never all resident
         host = any(x is not None and x.device.type == "cpu" for x in self.core.inputs) and \
             self.device.type == "cuda"
         self.core.streamer = _InputStreamer(self.sched, self.stages, self.core.inputs, self.device) \
-            if (host or self.stream_inputs) else None
+            if (host or self.stream_inputs) and self.core.lm is None else None
         if self.core.offload is not None and self.core.streamer is None:
             self.core.offload.exclude([x for x in self.core.inputs if x is not None])
         resident = {w.untyped_storage().data_ptr() for dl in self.model.layers.values() for w in dl.w.values()}
+        if self.core.lm is not None:
+            resident |= {self.lm_params.w_emb.untyped_storage().data_ptr(),
+                         self.lm_params.w_pos.untyped_storage().data_ptr()}
         if self.core.streamer is None:
             resident |= {x.untyped_storage().data_ptr() for x in self.core.inputs if x is not None}
         for st in self.stages.values():
@@ -1092,6 +1158,9 @@ class HelixRuntime:
         return 0 if chunked else post_stage(self.cfg.L - 1, self.cfg)
 
     def losses(self) -> list[float]:
+        if self.core.lm is not None:   # mean next-token cross-entropy per micro-batch
+            cnt = self.core.loss_count.cpu().tolist()
+            return [float(v) / max(1, c) for v, c in zip(self.sumsq.cpu().tolist(), cnt)]
         n = self.cfg.s * self.cfg.b * self.cfg.h
         return [float(v) / n for v in self.sumsq.cpu().tolist()]
 

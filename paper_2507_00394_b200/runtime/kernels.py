@@ -48,7 +48,8 @@ def gemm(a: torch.Tensor, a_mn: bool, b: torch.Tensor, b_mn: bool, out: torch.Te
     _lib.call("hx_gemm", a.data_ptr(), a.stride(0), int(a_mn), b.data_ptr(), b.stride(0), int(b_mn),
               out.data_ptr(), out.stride(0), M, N, K, epi, _ptr(aux),
               aux.stride(0) if aux is not None else 0, _ptr(out2),
-              out2.stride(0) if out2 is not None else 0, _stream())
+              out2.stride(0) if out2 is not None else 0, _stream(),
+              tag=f"{'T' if a_mn else 'N'}{'T' if b_mn else 'N'} {M}x{N}x{K} epi{epi}")
     return out
 
 

@@ -54,9 +54,20 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb
   nb = r / gm;
 }
 
-// Fused epilogue for 32 consecutive accumulator columns of one row.
+// The bf16 aux operand (residual or GeLU pre-activation) of 32 columns of one
+// row, loaded ahead of its accumulator so the load latency overlaps the MMAs.
+__device__ __forceinline__ void epilogue_aux_load(const GemmParams& p, int row, int col, uint4 (&a)[4]) {
+  if ((p.epi != HX_EPI_RESID_BF16 && p.epi != HX_EPI_DGELU) || row >= p.M) return;
+  const __nv_bfloat16* aux = reinterpret_cast<const __nv_bfloat16*>(p.aux) + static_cast<int64_t>(row) * p.ld_aux + col;
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (col + 8 * j + 8 <= p.N) a[j] = __ldg(reinterpret_cast<const uint4*>(aux + 8 * j));
+}
+
+// Fused epilogue for 32 consecutive accumulator columns of one row (aux, when
+// the epilogue has one, preloaded by epilogue_aux_load).
 __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row, int col,
-                                               const uint32_t (&acc)[32]) {
+                                               const uint32_t (&acc)[32], const uint4 (&pre)[4]) {
   if (row >= p.M) return;
   float v[32];
 #pragma unroll
@@ -83,9 +94,6 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row, int
     return;
   }
   __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out) + static_cast<int64_t>(row) * p.ldo + col;
-  const __nv_bfloat16* aux =
-      p.aux ? reinterpret_cast<const __nv_bfloat16*>(p.aux) + static_cast<int64_t>(row) * p.ld_aux + col
-            : nullptr;
   __nv_bfloat16* out2 =
       p.out2 ? reinterpret_cast<__nv_bfloat16*>(p.out2) + static_cast<int64_t>(row) * p.ldo2 + col
              : nullptr;
@@ -96,7 +104,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row, int
 #pragma unroll
     for (int i = 0; i < 8; ++i) x[i] = v[8 * j + i];
     if (epi == HX_EPI_RESID_BF16 || epi == HX_EPI_DGELU) {
-      uint4 a = *reinterpret_cast<const uint4*>(aux + 8 * j);
+      const uint4 a = pre[j];
       const uint32_t aw[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -267,14 +275,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       tc_fence_after();
       const int row = mb * GEMM_BM + sub * 32 + lane;
       const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(sub * 32) << 16);
+      uint4 aux_c[4], aux_n[4];
+      epilogue_aux_load(p, row, nb * BN, aux_c);
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         const int col = nb * BN + c * 32;
         if (col >= p.N) break;  // warp-uniform
+        if (c + 1 < BN / 32 && col + 32 < p.N) epilogue_aux_load(p, row, col + 32, aux_n);
         uint32_t r[32];
         tmem_ld32(taddr + c * 32, r);
         tmem_wait_ld();
-        epilogue_chunk(p, row, col, r);
+        epilogue_chunk(p, row, col, r, aux_c);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) aux_c[j] = aux_n[j];
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
@@ -304,8 +317,11 @@ constexpr int G2_STAGE_BYTES = G2_A_BYTES + G2_B_BYTES;
 constexpr int G2_BAR_OFFSET = G2_STAGES * G2_STAGE_BYTES;
 constexpr int G2_SMEM_BYTES = G2_BAR_OFFSET + 256 + 1024;
 
-template <bool A_MN, bool B_MN>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
+// EW epilogue warps (4 or 8): with 8, warps 4..7 drain accumulator columns
+// 0..127 and warps 8..11 columns 128..255 of their TMEM lane quadrant (warp & 3),
+// so the fused epilogues (GeLU, GeLU', residual) keep up with the MMAs.
+template <bool A_MN, bool B_MN, int EW>
+__global__ void __launch_bounds__(128 + 32 * EW, 1)
     gemm_2sm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                     const GemmParams p) {
   constexpr int BN = 256;
@@ -345,7 +361,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 256);  // epilogue threads of both CTAs
+      mbar_init(&tempty[a], 2 * 32 * EW);  // epilogue threads of both CTAs
     }
     fence_barrier_init();
   }
@@ -425,24 +441,32 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   } else if (warp >= 4) {
     // ---------------- epilogue (both CTAs): this CTA's 128 rows of the 256 x 256 tile
     const int sub = warp & 3;
+    constexpr int CPW = (BN / 32) * 4 / EW;     // 32-column chunks per warp
+    const int c0 = ((warp - 4) / 4) * CPW;      // this warp's first chunk
     const uint32_t tempty_leader0 = mapa_shared(&tempty[0], 0);
     int it = 0;
     for (int u = first; u < num_units; u += stride, ++it) {
       int mp, nb;
       tile_coords(u / S, num_m / 2, num_n, mp, nb, p.group_m);
       const int acc = it & 1;
+      const int row = (2 * mp + rank) * GEMM_BM + sub * 32 + lane;
+      // the first chunk's aux is loaded before the accumulator is ready
+      uint4 aux_c[4], aux_n[4];
+      epilogue_aux_load(p, row, nb * BN + c0 * 32, aux_c);
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
-      const int row = (2 * mp + rank) * GEMM_BM + sub * 32 + lane;
       const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(sub * 32) << 16);
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = c0; c < c0 + CPW; ++c) {
         const int col = nb * BN + c * 32;
         if (col >= p.N) break;  // warp-uniform
+        if (c + 1 < c0 + CPW && col + 32 < p.N) epilogue_aux_load(p, row, col + 32, aux_n);
         uint32_t r[32];
         tmem_ld32(taddr + c * 32, r);
         tmem_wait_ld();
-        epilogue_chunk(p, row, col, r);
+        epilogue_chunk(p, row, col, r, aux_c);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) aux_c[j] = aux_n[j];
       }
       tc_fence_before();
       mbar_arrive_cluster(tempty_leader0 + acc * 8);
@@ -456,10 +480,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
 }
 
-template <bool A_MN, bool B_MN>
-static cudaError_t launch_gemm_2sm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
-                                   int num_sms, cudaStream_t stream) {
-  auto kern = gemm_2sm_kernel<A_MN, B_MN>;
+template <bool A_MN, bool B_MN, int EW>
+static cudaError_t launch_gemm_2sm_ew(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
+                                      int num_sms, cudaStream_t stream) {
+  auto kern = gemm_2sm_kernel<A_MN, B_MN, EW>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G2_SMEM_BYTES);
@@ -470,7 +494,7 @@ static cudaError_t launch_gemm_2sm(const CUtensorMap& ta, const CUtensorMap& tb,
   int grid = 2 * (pairs < num_sms / 2 ? pairs : num_sms / 2);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.blockDim = dim3(128 + 32 * EW);
   cfg.dynamicSmemBytes = G2_SMEM_BYTES;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
@@ -481,6 +505,15 @@ static cudaError_t launch_gemm_2sm(const CUtensorMap& ta, const CUtensorMap& tb,
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, ta, tb, p);
+}
+
+// 8 epilogue warps by default; HX_GEMM_EPI_WARPS=4 selects the round-1 layout (A/B runs).
+template <bool A_MN, bool B_MN>
+static cudaError_t launch_gemm_2sm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
+                                   int num_sms, cudaStream_t stream) {
+  static const int ew = getenv("HX_GEMM_EPI_WARPS") ? atoi(getenv("HX_GEMM_EPI_WARPS")) : 8;
+  if (ew == 4) return launch_gemm_2sm_ew<A_MN, B_MN, 4>(ta, tb, p, num_sms, stream);
+  return launch_gemm_2sm_ew<A_MN, B_MN, 8>(ta, tb, p, num_sms, stream);
 }
 
 // ------------------------------------------------------------------ host side

@@ -53,6 +53,8 @@ def main():
     ap.add_argument("--regen-pre-x", action="store_true")
     ap.add_argument("--stash-budget-gb", type=float, default=None)
     ap.add_argument("--iters", type=int, default=2, help="the last one is measured")
+    ap.add_argument("--stream-inputs", action="store_true",
+                    help="keep the inputs in pinned host memory (the runtime's input streamer)")
     args = ap.parse_args()
 
     wl = dict(WORKLOADS[args.workload])
@@ -82,6 +84,8 @@ def main():
         T = cfg.s * cfg.b
         inputs = [torch.randn(T, cfg.h, generator=ig, device=dev).to(torch.bfloat16) if stage == first else None
                   for _ in range(cfg.m)]
+        if args.stream_inputs:
+            inputs = [None if x is None else x.cpu().pin_memory() for x in inputs]
         try:
             for it in range(args.iters):
                 torch.cuda.synchronize()
@@ -104,7 +108,8 @@ def main():
         span = max(e for _s, e in tl.values()) - min(s for s, _e in tl.values())
         table = measured_durations(sched, tl) if not chunked else None
         st = rt.stages[stage]
-        pl = plan(sched, stage, args.mlp_chunk, regen_pre_x=args.regen_pre_x, durations=table or units)
+        pl = plan(sched, stage, args.mlp_chunk, regen_pre_x=args.regen_pre_x, durations=table or units,
+                  stream_inputs=args.stream_inputs)
         out = {
             "probe": "stage", "workload": args.workload, "L": cfg.L, "h": cfg.h, "s": cfg.s, "p": cfg.p, "m": cfg.m,
             "method": args.method, "stage": stage, "mlp_chunk": args.mlp_chunk, "regen_pre_x": args.regen_pre_x,

@@ -73,6 +73,9 @@ def parse():
     ap.add_argument("--trace-out", default=None,
                     help="write the measured per-task device timeline of one iteration as a Chrome "
                          "trace (<prefix>.trace.json) and CSV (<prefix>.csv), reference schema")
+    ap.add_argument("--lm-vocab", type=int, default=None,
+                    help="language-model mode (paper 4.6, runtime/lm.py): token inputs, word + position "
+                         "embeddings and the tied head with the loss in backward, vocabulary V")
     ap.add_argument("--compare-1f1b", choices=["auto", "yes", "no"], default="auto",
                     help="also time the same-kernel 1F1B schedule on the same model / inputs "
                          "(auto: yes, except for the host-offload workload gpt7b_128k)")
@@ -543,14 +546,21 @@ def bench_gpu(args, wl, world: int, rank: int, local: int) -> None:
             torch.cuda.synchronize()
             free, _total = torch.cuda.mem_get_info(dev)
             budget = max(0, free - 40 * cfg.s * cfg.b * cfg.h * 2)
+        lm_kw = {}
+        if args.lm_vocab:
+            from paper_2507_00394_b200.runtime.lm import LMSpec
+            lm_kw = {"lm": LMSpec(args.lm_vocab)}
         return HelixRuntime(schedule, DeviceModel(layers), args.mlp_chunk,
                             "distributed" if world > 1 else "replay", dev,
-                            rank=rank if world > 1 else None, groups=groups, stash_budget_bytes=budget)
+                            rank=rank if world > 1 else None, groups=groups, stash_budget_bytes=budget, **lm_kw)
 
     rt = build_runtime(sched)
     T = cfg.s * cfg.b
     ig = torch.Generator(device=dev).manual_seed(1)
-    inputs = [torch.randn(T, cfg.h, generator=ig, device=dev).to(torch.bfloat16) for _ in range(cfg.m)]
+    if args.lm_vocab:   # token ids (N(0,1) activations otherwise)
+        inputs = [torch.randint(0, args.lm_vocab, (cfg.s, cfg.b), generator=ig, device=dev) for _ in range(cfg.m)]
+    else:
+        inputs = [torch.randn(T, cfg.h, generator=ig, device=dev).to(torch.bfloat16) for _ in range(cfg.m)]
 
     def barrier():
         if world > 1:
@@ -674,7 +684,8 @@ def bench_gpu(args, wl, world: int, rank: int, local: int) -> None:
         e2e_ev0.record()
         for _ in range(args.steps):
             rt.run(host)
-            h2d0 += rt.core.streamer.h2d_bytes
+            h2d0 += rt.core.streamer.h2d_bytes if rt.core.streamer is not None else \
+                sum(x.numel() * 4 for x in host)       # LM mode: int32 token ids
             got = rt.sumsq.cpu()  # D2H read of the step's losses (sync)
         h2d = h2d0 // args.steps
         e2e_ev1.record()
@@ -814,6 +825,8 @@ def bench_gpu(args, wl, world: int, rank: int, local: int) -> None:
 
     if rank == 0:
         fpt = b200_flops_per_token(cfg)
+        if args.lm_vocab:   # tied head: logits, dz, dW_emb GEMMs (2hV FLOPs each per token)
+            fpt += 6 * cfg.h * args.lm_vocab
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -821,6 +834,7 @@ def bench_gpu(args, wl, world: int, rank: int, local: int) -> None:
             "config": {"workload": args.workload, **wl, "p": p, "m": cfg.m, "method": args.method,
                        "n_gpus": world,
                        "mlp_chunk": args.mlp_chunk, "parallelism": f"pp{p} (one helix stage per GPU)",
+                       **({"lm_vocab": args.lm_vocab} if args.lm_vocab else {}),
                        "l2": "inputs/activations >> L2 (134 MB per tensor), no flush"},
             "mfu": value * fpt / (world * float(peaks["bf16_tflops"]) * 1e12),
             "model_flops_per_token": fpt,

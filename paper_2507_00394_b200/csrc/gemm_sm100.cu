@@ -507,11 +507,15 @@ static cudaError_t launch_gemm_2sm_ew(const CUtensorMap& ta, const CUtensorMap& 
   return cudaLaunchKernelEx(&cfg, kern, ta, tb, p);
 }
 
-// 8 epilogue warps by default; HX_GEMM_EPI_WARPS=4 selects the round-1 layout (A/B runs).
+// Epilogue warps per epilogue (HX_GEMM_EPI_WARPS=4/8 forces one for A/B runs).
+// Measured in the GPT-1.3B/32k bench step (GEMM time per step 391 -> 378 ms):
+// W2^T * GeLU' (reads m1) 0.72 -> 1.00 PFLOP/s with 8 warps; W1 + GeLU (writes
+// m1 and g) 1.03 -> 0.90 PFLOP/s, so it keeps 4.
 template <bool A_MN, bool B_MN>
 static cudaError_t launch_gemm_2sm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
                                    int num_sms, cudaStream_t stream) {
-  static const int ew = getenv("HX_GEMM_EPI_WARPS") ? atoi(getenv("HX_GEMM_EPI_WARPS")) : 8;
+  static const int forced = getenv("HX_GEMM_EPI_WARPS") ? atoi(getenv("HX_GEMM_EPI_WARPS")) : 0;
+  const int ew = forced ? forced : (p.epi == HX_EPI_GELU ? 4 : 8);
   if (ew == 4) return launch_gemm_2sm_ew<A_MN, B_MN, 4>(ta, tb, p, num_sms, stream);
   return launch_gemm_2sm_ew<A_MN, B_MN, 8>(ta, tb, p, num_sms, stream);
 }

@@ -182,6 +182,21 @@ class DeviceModel:
             dl.zero_grads(zero_fn)
 
 
+_SIDE_STREAMS: dict[tuple, torch.cuda.Stream] = {}
+
+
+def side_stream(device, role: str) -> torch.cuda.Stream:
+    """One persistent CUDA stream per (device, role): per-stage compute streams,
+    the receive stream, the input streamer's and the offloader's copy streams.
+    The caching allocator keeps freed blocks per stream, so a fresh stream per
+    call / iteration would miss its cache and cudaMalloc anew every time."""
+    key = (str(torch.device(device)), role)
+    st = _SIDE_STREAMS.get(key)
+    if st is None:
+        st = _SIDE_STREAMS[key] = torch.cuda.Stream(device=device)
+    return st
+
+
 class HostInput:
     """Stash placeholder for a micro-batch input (layer 0's x) that stays in
     host memory while the input streamer is active; counted like the tensor
@@ -209,7 +224,7 @@ class _InputStreamer:
         self.host = host
         self.device = device
         self.cuda = device.type == "cuda"
-        self.stream = torch.cuda.Stream(device=device) if self.cuda else None
+        self.stream = side_stream(device, "inputs") if self.cuda else None
         self.lookahead = lookahead
         self.ready: dict[str, tuple] = {}
         self.uses: dict[int, list[tuple[int, str, int]]] = {}
@@ -594,12 +609,14 @@ def _replay(core: _Core, timer: _Timer) -> None:
         raise ExecutionError(f"undelivered payloads: {sorted(transit)}")
 
 
+
+
 def _multistream(core: _Core, timer: _Timer) -> None:
     """One CUDA stream per stage on one GPU; host issues in replay order, the
     device overlaps stages.  Cross-stage payloads are ordered by events."""
     tasks, order = core.tasks, core.sched.per_stage_order
     main = torch.cuda.current_stream()
-    streams = {si: torch.cuda.Stream() for si in core.stages}
+    streams = {si: side_stream(main.device, f"stage{si}") for si in core.stages}
     start = torch.cuda.Event()
     start.record(main)
     for s in streams.values():
@@ -786,7 +803,7 @@ class _Distributed:
                 send_cap = None
         self.sends: dict[int, _SendQueue] = {}
         self.send_cap = send_cap
-        self.comm_stream = torch.cuda.Stream(device=st.device) if self.cuda else None
+        self.comm_stream = side_stream(st.device, "recv") if self.cuda else None
         self.posted: dict[str, tuple[list, dict]] = {}    # rid -> (works, payload)
         self.next_recv: dict[int, int] = {}               # src -> index into recv_seq
         self.recv_index = {rid: (src, k) for (src, dst), seq in self.plan.recv_seq.items()

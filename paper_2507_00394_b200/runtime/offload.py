@@ -69,8 +69,10 @@ class StashOffloader:
         self.budget = int(budget_bytes)
         self.min_bytes = min_bytes
         self.weight_ptrs = {w.untyped_storage().data_ptr() for w in weights}
-        self.d2h = torch.cuda.Stream()
-        self.h2d = torch.cuda.Stream()
+        from .executor import side_stream
+        dev = torch.cuda.current_device()
+        self.d2h = side_stream(dev, "offload_d2h")
+        self.h2d = side_stream(dev, "offload_h2d")
         self.pool: dict[tuple, list[tuple[torch.Tensor, torch.cuda.Event | None]]] = {}
         # stage -> serial -> entry; resident tensors are found by object identity
         # (id(tensor) -> serial, validated with `is`): device addresses and ids are

@@ -135,6 +135,38 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row, int
   }
 }
 
+// bf16 epilogues (STORE / RESID / GELU / DGELU) of 32 accumulator columns of
+// one row, packed to bf16 pairs: o = the output, o2 = GeLU(output) for GELU.
+__device__ __forceinline__ void epilogue_values(int epi, const uint32_t (&acc)[32], const uint4 (&pre)[4],
+                                                uint32_t (&o)[16], uint32_t (&o2)[16]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    float x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = __uint_as_float(acc[8 * j + i]);
+    if (epi == HX_EPI_RESID_BF16 || epi == HX_EPI_DGELU) {
+      const uint32_t aw[4] = {pre[j].x, pre[j].y, pre[j].z, pre[j].w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 f = unpack_bf16(aw[i]);
+        if (epi == HX_EPI_RESID_BF16) {
+          x[2 * i] += f.x;
+          x[2 * i + 1] += f.y;
+        } else {
+          x[2 * i] *= gelu_erf_grad(f.x);
+          x[2 * i + 1] *= gelu_erf_grad(f.y);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o[4 * j + i] = pack_bf16(x[2 * i], x[2 * i + 1]);
+    if (epi == HX_EPI_GELU) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) o2[4 * j + i] = pack_bf16(gelu_erf(x[2 * i]), gelu_erf(x[2 * i + 1]));
+    }
+  }
+}
+
 // CL = true: clusters of 2 CTAs on vertically adjacent M-blocks that share the
 // B panel.  Each CTA TMA-loads its own A tile and HALF of the B tile, multicast
 // to both CTAs, so L2->SM traffic per MMA drops from (A + B) to (A + B/2): 48 ->
@@ -314,7 +346,11 @@ constexpr int G2_STAGES = 6;
 constexpr int G2_A_BYTES = GEMM_BM * GEMM_BK * 2;   // 16 KB: this CTA's 128 rows
 constexpr int G2_B_BYTES = 128 * GEMM_BK * 2;       // 16 KB: this CTA's 128 of 256 columns
 constexpr int G2_STAGE_BYTES = G2_A_BYTES + G2_B_BYTES;
-constexpr int G2_BAR_OFFSET = G2_STAGES * G2_STAGE_BYTES;
+// bf16 epilogues stage each warp's 32 x 32 output chunk (SWIZZLE_64B) here and
+// TMA-store it: per warp 2 buffers x (1 or 2 outputs) x 2 KB, 32 KB in all
+constexpr int G2_STG_OFFSET = G2_STAGES * G2_STAGE_BYTES;
+constexpr int G2_STG_BYTES = 32768;
+constexpr int G2_BAR_OFFSET = G2_STG_OFFSET + G2_STG_BYTES;
 constexpr int G2_SMEM_BYTES = G2_BAR_OFFSET + 256 + 1024;
 
 // EW epilogue warps (4 or 8): with 8, warps 4..7 drain accumulator columns
@@ -323,6 +359,7 @@ constexpr int G2_SMEM_BYTES = G2_BAR_OFFSET + 256 + 1024;
 template <bool A_MN, bool B_MN, int EW>
 __global__ void __launch_bounds__(128 + 32 * EW, 1)
     gemm_2sm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+                    const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_c2,
                     const GemmParams p) {
   constexpr int BN = 256;
   extern __shared__ uint8_t smem_raw[];
@@ -444,12 +481,20 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
     constexpr int CPW = (BN / 32) * 4 / EW;     // 32-column chunks per warp
     const int c0 = ((warp - 4) / 4) * CPW;      // this warp's first chunk
     const uint32_t tempty_leader0 = mapa_shared(&tempty[0], 0);
+    // bf16 outputs leave through smem + TMA stores (coalesced, async); fp32 ones
+    // (weight-gradient accumulation) keep the per-row path
+    const int nout = p.epi == HX_EPI_GELU ? 2 : 1;
+    const bool tma_out = p.tma_store && p.epi != HX_EPI_ACC_F32 && p.epi != HX_EPI_STORE_F32 &&
+                         nout * 2 * 2048 * EW <= G2_STG_BYTES;
+    uint8_t* stg = smem + G2_STG_OFFSET + (warp - 4) * (G2_STG_BYTES / EW);
+    int kbuf = 0;
     int it = 0;
     for (int u = first; u < num_units; u += stride, ++it) {
       int mp, nb;
       tile_coords(u / S, num_m / 2, num_n, mp, nb, p.group_m);
       const int acc = it & 1;
-      const int row = (2 * mp + rank) * GEMM_BM + sub * 32 + lane;
+      const int row0 = (2 * mp + rank) * GEMM_BM + sub * 32;
+      const int row = row0 + lane;
       // the first chunk's aux is loaded before the accumulator is ready
       uint4 aux_c[4], aux_n[4];
       epilogue_aux_load(p, row, nb * BN + c0 * 32, aux_c);
@@ -464,7 +509,32 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
         uint32_t r[32];
         tmem_ld32(taddr + c * 32, r);
         tmem_wait_ld();
-        epilogue_chunk(p, row, col, r, aux_c);
+        if (tma_out) {
+          uint32_t o[16], o2[16];
+          epilogue_values(p.epi, r, aux_c, o, o2);
+          uint8_t* buf = stg + (kbuf & 1) * (nout * 2048);
+          if (lane == 0) bulk_wait_read<1>();  // the store that last read this buffer is done
+          __syncwarp();
+          // row `lane` of the 32 x 64-byte box, SWIZZLE_64B: 16-byte chunk j at j ^ ((row >> 1) & 3)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int off = lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4);
+            *reinterpret_cast<uint4*>(buf + off) = make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+            if (nout == 2)
+              *reinterpret_cast<uint4*>(buf + 2048 + off) =
+                  make_uint4(o2[4 * j], o2[4 * j + 1], o2[4 * j + 2], o2[4 * j + 3]);
+          }
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tm_c, buf, col, row0);
+            if (nout == 2) tma_store_2d(&tm_c2, buf + 2048, col, row0);
+            bulk_commit();
+          }
+          ++kbuf;
+        } else {
+          epilogue_chunk(p, row, col, r, aux_c);
+        }
 #pragma unroll
         for (int j = 0; j < 4; ++j) aux_c[j] = aux_n[j];
       }
@@ -472,6 +542,7 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
       mbar_arrive_cluster(tempty_leader0 + acc * 8);
     }
   }
+  if (warp >= 4 && lane == 0) bulk_wait_all();  // epilogue TMA stores have left smem
   __syncthreads();
   cluster_sync();  // the peer's smem / barriers stay valid until both CTAs are done
   if (warp == 2) {
@@ -483,6 +554,13 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
 template <bool A_MN, bool B_MN, int EW>
 static cudaError_t launch_gemm_2sm_ew(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
                                       int num_sms, cudaStream_t stream) {
+  // output tensor maps of the TMA-store epilogue (bf16 [M, N], 32 x 32 boxes)
+  CUtensorMap tc = ta, tc2 = ta;
+  if (p.epi != HX_EPI_ACC_F32 && p.epi != HX_EPI_STORE_F32) {
+    cudaError_t e = make_tma_2d_sw64(&tc, p.out, p.M, p.N, p.ldo, 32, 32);
+    if (e == cudaSuccess && p.epi == HX_EPI_GELU) e = make_tma_2d_sw64(&tc2, p.out2, p.M, p.N, p.ldo2, 32, 32);
+    if (e != cudaSuccess) return e;
+  }
   auto kern = gemm_2sm_kernel<A_MN, B_MN, EW>;
   static bool configured = false;
   if (!configured) {
@@ -504,7 +582,7 @@ static cudaError_t launch_gemm_2sm_ew(const CUtensorMap& ta, const CUtensorMap& 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, ta, tb, p);
+  return cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tc2, p);
 }
 
 // Epilogue warps per epilogue (HX_GEMM_EPI_WARPS=4/8 forces one for A/B runs).
@@ -652,6 +730,8 @@ cudaError_t gemm_launch(const GemmOperand& a, const GemmOperand& b, const GemmPa
   // weight gradient: 64 pairs); only tiny GEMMs stay on single CTAs
   if (cl_mode == 2 && num_m % 2 == 0 && p.N > 128 && pairs >= 32) {
     GemmParams q = p;
+    static const int tma_store = getenv("HX_GEMM_TMA_STORE") ? atoi(getenv("HX_GEMM_TMA_STORE")) : 1;
+    q.tma_store = tma_store;
     q.ksplit = pick_ksplit(p, pairs, num_sms / 2);
     q.group_m = pick_group(p, num_m / 2, (p.N + 255) / 256, (num_sms / 2) / q.ksplit);
     e = b.mn ? make_tma_2d(&tb, b.ptr, p.K, p.N, b.ld, 64, 64) : make_tma_2d(&tb, b.ptr, p.N, p.K, b.ld, 64, 128);

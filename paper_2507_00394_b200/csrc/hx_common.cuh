@@ -239,6 +239,12 @@ HX_DEVICE void tma_reduce_add_3d(const CUtensorMap* map, const void* src, int x,
       : "memory");
 }
 HX_DEVICE void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+HX_DEVICE void tma_store_2d(const CUtensorMap* map, const void* src, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(x), "r"(y)
+               : "memory");
+}
 // Wait until at most N of this thread's bulk groups still read their smem source.
 template <int N>
 HX_DEVICE void bulk_wait_read() {

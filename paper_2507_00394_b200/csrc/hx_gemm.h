@@ -26,12 +26,18 @@ struct GemmParams {
   int ldo2;
   int ksplit;            // K slices per tile (pair kernel, ACC_F32 only; set by gemm_launch)
   int group_m;           // tile-raster M-group in pair-rows (pair kernel; set by gemm_launch)
+  int tma_store;         // bf16 outputs via smem + TMA store (pair kernel; HX_GEMM_TMA_STORE=0 disables)
 };
 
 // 2-D bf16 tensor map over a row-major [rows, cols] matrix with row stride ld,
 // SWIZZLE_128B, box {box_cols, box_rows}.  OOB reads are zero-filled.
 cudaError_t make_tma_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint64_t ld,
                         uint32_t box_cols, uint32_t box_rows);
+
+// 2-D bf16 tensor map as make_tma_2d but SWIZZLE_64B (box_cols * 2 bytes = 64):
+// the GEMM epilogue's TMA stores of 32-column row chunks.
+cudaError_t make_tma_2d_sw64(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint64_t ld,
+                             uint32_t box_cols, uint32_t box_rows);
 
 // 3-D bf16 tensor map over activations stored token-major [s][b][ld]: dims
 // {cols, b, s}, box {box_cols, 1, box_rows} (one batch column, box_rows tokens).

@@ -95,6 +95,34 @@ def test_attention_delta_matches_rowsum():
     assert rel_err(delta, want) < 1e-5
 
 
+@pytest.mark.parametrize("T,Kd,N", [(4096, 512, 1024), (4000, 256, 1000), (8192, 1024, 2056)])
+def test_gemm_pair_kernel_epilogues(T, Kd, N):
+    # shapes with >= 32 tile pairs take the cta_group::2 kernel, whose bf16 epilogues
+    # (store, +residual, GeLU with its pre-activation, x GeLU') leave through smem and
+    # TMA stores; ragged M and N exercise the clipped boxes.  tol 1e-2 of max|ref|
+    x, w = rnd(T, Kd, seed=21), rnd(Kd, N, scale=Kd ** -0.5, seed=22)
+    ref = x.float() @ w.float()
+    y = K.linear(x, w)
+    m1 = torch.empty(T, N, dtype=torch.bfloat16, device=DEV)
+    g = torch.empty_like(m1)
+    K.linear_gelu(x, w, m1, g)
+    resid = rnd(T, N, seed=23)
+    yr = K.linear_resid(x, w, resid)
+    w2 = rnd(Kd, N, scale=N ** -0.5, seed=24)
+    dy = rnd(T, N, seed=25)
+    m1b = rnd(T, Kd, seed=26)
+    dm = torch.empty(T, Kd, dtype=torch.bfloat16, device=DEV)
+    K.linear_dx_dgelu(dy, w2, m1b, dm)
+    torch.cuda.synchronize()
+    assert rel_err(y, ref) < 1e-2
+    assert rel_err(m1, ref) < 1e-2
+    assert rel_err(g, torch.nn.functional.gelu(ref)) < 1e-2
+    assert rel_err(yr, ref + resid.float()) < 1e-2
+    mf = m1b.float()
+    gelu_grad = 0.5 * (1 + torch.erf(mf / math.sqrt(2))) + mf * torch.exp(-0.5 * mf * mf) / math.sqrt(2 * math.pi)
+    assert rel_err(dm, (dy.float() @ w2.float().t()) * gelu_grad) < 1e-2
+
+
 def test_gemm_epilogues():
     T, Kd, N = 512, 256, 1024
     x, w = rnd(T, Kd, seed=7), rnd(Kd, N, scale=Kd ** -0.5, seed=8)

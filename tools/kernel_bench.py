@@ -80,6 +80,15 @@ def main():
                 wt = torch.empty(kin, nout, dtype=bf, device=dev)
                 out(f"cublas_dw_{name}", timed(lambda: torch.matmul(a.t(), dy, out=wt), args.reps), fl,
                     M=kin, N=nout, K=T)
+            if name == "mlp_w1":   # fused GeLU epilogue: writes m1 and g
+                g = torch.empty_like(y)
+                out("fwd_mlp_w1_gelu", timed(lambda: K.linear_gelu(a, w, y, g), args.reps), fl, M=T, N=nout, K=kin)
+                del g
+            if name == "mlp_w2":   # fused GeLU' epilogue: reads the pre-activation m1
+                m1 = torch.randn(T, kin, device=dev).to(bf)
+                out("dx_mlp_w2_dgelu", timed(lambda: K.linear_dx_dgelu(dy, w, m1, dx), args.reps), fl,
+                    M=T, N=kin, K=nout)
+                del m1
             del w, a, y, dy, dx, acc
         del x
         torch.cuda.empty_cache()

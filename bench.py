@@ -799,6 +799,14 @@ def bench_gpu(args, wl, world: int, rank: int, local: int) -> None:
                              "attn_bwd_ms": iso_bwd_ms, "attn_bwd_frac": bwd_fl / (iso_bwd_ms / 1e3) / 1e12 / burst,
                              "attn_fwd_ms": iso_fwd_ms, "attn_fwd_frac": fwd_fl / (iso_fwd_ms / 1e3) / 1e12 / burst},
                 "flops_convention": "causal: fwd 2*b*n*s^2*d, bwd 2.5x fwd"}
+        # the sustained peak was measured at its own (power-capped) median clock;
+        # rescaled to the clock this step ran at, the fraction is clock-neutral
+        peak_mhz = (peaks.get("clocks_under_load") or {}).get("sm_mhz_median")
+        if peak_mhz and clk.get("sm_mhz"):
+            scaled_peak = sustained * float(clk["sm_mhz"]) / float(peak_mhz)
+            roof["frac_at_step_clock"] = ach / scaled_peak
+            roof["peak_at_step_clock"] = {"value": scaled_peak, "how": f"bf16_tflops_sustained x step "
+                                          f"{clk['sm_mhz']:.0f} MHz / its {peak_mhz:.0f} MHz median"}
         del qkv, o, lse, do, dqkv, delta, dq
 
     # like-for-like pair at BASELINE config 1 (the reference arm's configuration)

@@ -484,8 +484,10 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
     // bf16 outputs leave through smem + TMA stores (coalesced, async); fp32 ones
     // (weight-gradient accumulation) keep the per-row path
     const int nout = p.epi == HX_EPI_GELU ? 2 : 1;
+    // staging buffers per warp: 2 (double-buffered) if they fit, else 1
+    const int nbuf = nout * 2 * 2048 * EW <= G2_STG_BYTES ? 2 : 1;
     const bool tma_out = p.tma_store && p.epi != HX_EPI_ACC_F32 && p.epi != HX_EPI_STORE_F32 &&
-                         nout * 2 * 2048 * EW <= G2_STG_BYTES;
+                         nout * nbuf * 2048 * EW <= G2_STG_BYTES;
     uint8_t* stg = smem + G2_STG_OFFSET + (warp - 4) * (G2_STG_BYTES / EW);
     int kbuf = 0;
     int it = 0;
@@ -512,8 +514,11 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
         if (tma_out) {
           uint32_t o[16], o2[16];
           epilogue_values(p.epi, r, aux_c, o, o2);
-          uint8_t* buf = stg + (kbuf & 1) * (nout * 2048);
-          if (lane == 0) bulk_wait_read<1>();  // the store that last read this buffer is done
+          uint8_t* buf = stg + (nbuf == 2 ? (kbuf & 1) * (nout * 2048) : 0);
+          if (lane == 0) {  // the store that last read this buffer is done
+            if (nbuf == 2) bulk_wait_read<1>();
+            else bulk_wait_read<0>();
+          }
           __syncwarp();
           // row `lane` of the 32 x 64-byte box, SWIZZLE_64B: 16-byte chunk j at j ^ ((row >> 1) & 3)
 #pragma unroll
@@ -585,15 +590,18 @@ static cudaError_t launch_gemm_2sm_ew(const CUtensorMap& ta, const CUtensorMap& 
   return cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tc2, p);
 }
 
-// Epilogue warps per epilogue (HX_GEMM_EPI_WARPS=4/8 forces one for A/B runs).
-// Measured in the GPT-1.3B/32k bench step (GEMM time per step 391 -> 378 ms):
-// W2^T * GeLU' (reads m1) 0.72 -> 1.00 PFLOP/s with 8 warps; W1 + GeLU (writes
-// m1 and g) 1.03 -> 0.90 PFLOP/s, so it keeps 4.
+// Epilogue warps (HX_GEMM_EPI_WARPS=4/8 forces one for A/B runs; 8 by default).
+// Measured in the GPT-1.3B/32k bench step: W2^T * GeLU' (reads m1) 0.72 -> 1.00
+// PFLOP/s with 8 warps.  W1 + GeLU (writes m1 and g) was slower with 8 warps on
+// the per-row store path (1.03 -> 0.90); with the TMA-store epilogue (8 warps,
+// single-buffered staging for its two outputs) it is faster than with 4
+// (HX_GEMM_GELU_WARPS A/B: 375 vs 402 ms of GEMM per step, +1.3% tokens/s).
 template <bool A_MN, bool B_MN>
 static cudaError_t launch_gemm_2sm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
                                    int num_sms, cudaStream_t stream) {
   static const int forced = getenv("HX_GEMM_EPI_WARPS") ? atoi(getenv("HX_GEMM_EPI_WARPS")) : 0;
-  const int ew = forced ? forced : (p.epi == HX_EPI_GELU ? 4 : 8);
+  static const int gelu_ew = getenv("HX_GEMM_GELU_WARPS") ? atoi(getenv("HX_GEMM_GELU_WARPS")) : 8;
+  const int ew = forced ? forced : (p.epi == HX_EPI_GELU ? gelu_ew : 8);
   if (ew == 4) return launch_gemm_2sm_ew<A_MN, B_MN, 4>(ta, tb, p, num_sms, stream);
   return launch_gemm_2sm_ew<A_MN, B_MN, 8>(ta, tb, p, num_sms, stream);
 }

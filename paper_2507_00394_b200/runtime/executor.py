@@ -769,6 +769,34 @@ class _SendQueue:
         return len(self.q)
 
 
+class _WqkvDedupe:
+    """Receiver-side dedupe of the W_qkv copies in ``pa`` payloads.
+
+    Every pre -> attention payload carries the layer's qkv weight
+    (``P/costs.py:139-150``; 3h^2 bf16, 100 MB at h=4096), and the attention
+    stash keeps it for the backward.  The weights do not change within an
+    iteration, so all copies of one layer that a stage receives are equal: the
+    first is kept (weakly referenced) and later payloads of that layer reuse
+    it, freeing their buffers.  The wire contract (``comm_volume``) is
+    unchanged; at 7B/128k p=8 a rank holds 32 instead of 64 copies (3.2 GB)."""
+
+    def __init__(self):
+        import weakref
+        self.cache: "weakref.WeakValueDictionary[int, torch.Tensor]" = weakref.WeakValueDictionary()
+
+    def dedupe(self, rid: str, payload: dict) -> dict:
+        w = payload.get("qkv_weight")
+        if w is None or _edge_tag(rid) != "pa":
+            return payload
+        layer = int(rid.split(".")[2][1:])
+        prev = self.cache.get(layer)
+        if prev is None:
+            self.cache[layer] = w
+        else:
+            payload["qkv_weight"] = prev
+        return payload
+
+
 class _Distributed:
     """Rank r executes stage r; payloads move over NCCL (or gloo on CPU tests).
 
@@ -804,6 +832,7 @@ class _Distributed:
         self.sends: dict[int, _SendQueue] = {}
         self.send_cap = send_cap
         self.comm_stream = side_stream(st.device, "recv") if self.cuda else None
+        self.wqkv = _WqkvDedupe()
         self.posted: dict[str, tuple[list, dict]] = {}    # rid -> (works, payload)
         self.next_recv: dict[int, int] = {}               # src -> index into recv_seq
         self.recv_index = {rid: (src, k) for (src, dst), seq in self.plan.recv_seq.items()
@@ -852,7 +881,7 @@ class _Distributed:
             cur = torch.cuda.current_stream()
             for t in payload.values():
                 t.record_stream(cur)
-        return payload
+        return self.wqkv.dedupe(rid, payload)
 
     def live_sends(self) -> int:
         return sum(len(q) for q in self.sends.values())
@@ -917,6 +946,7 @@ class _Loopback:
         self.send_cap = send_cap
         st = core.stages[rank]
         self.gen = torch.Generator(device=st.device).manual_seed(seed)
+        self.wqkv = _WqkvDedupe()
         order = core.sched.per_stage_order[rank]
         self.needs: list[list[str]] = []
         seen: set[str] = set()
@@ -937,7 +967,7 @@ class _Loopback:
                 (1e-3 if name.startswith("d_") or name == "delta" else 1.0)
             buf.normal_(0.0, scale, generator=self.gen)
             out[name] = buf
-        return out
+        return self.wqkv.dedupe(rid, out)
 
     def run(self, timer: _Timer) -> None:
         core, r = self.core, self.rank

@@ -135,8 +135,8 @@ def stash_walk(sched: Schedule, stage: int, dt: Dtypes = Dtypes(), regen_pre_x: 
                 t.append((local(f"ln:{l}.{i}", "pre", l, i), act))
                 if not rc:
                     t.append((f"qkv:{l}.{i}", 3 * act))
-                if stage_of("pre", l, i) != stage:
-                    t.append((f"wqkv:{l}.{i}@rx", 3 * h * h * A))
+                if stage_of("pre", l, i) != stage:   # received copy, one per layer (executor _WqkvDedupe)
+                    t.append((f"wqkv:{l}@rx", 3 * h * h * A))
             else:
                 t.append((local(f"qkv:{l}.{i}", "pre", l, i), 3 * act))
             t.append((f"lse:{l}.{i}", lse))

@@ -340,7 +340,9 @@ def load_peaks() -> dict:
 
 def profile_traffic(kernel: str) -> float | None:
     """DRAM bytes per launch of ``kernel`` from the committed ncu --set full summary."""
-    p = ROOT / "profiles" / "ncu_summary.json"
+    p = ROOT / "profiles" / "ncu_summary_r02.json"   # this round's capture of the current kernels
+    if not p.exists():
+        p = ROOT / "profiles" / "ncu_summary.json"
     if not p.exists():
         return None
     try:

@@ -352,6 +352,34 @@ def profile_traffic(kernel: str) -> float | None:
         return None
 
 
+def baseline_memory_plan() -> dict:
+    """Worst-rank device memory of BASELINE configs 2-4 at their GPU counts
+    (runtime/memplan.py; 180 GB B200) and the host memory the FILO offloader
+    needs: the plan the stage probes check on the B200."""
+    from paper_2507_00394_b200 import ModelConfig, generate
+    from paper_2507_00394_b200.costs import DurationTable
+    from paper_2507_00394_b200.runtime.memplan import GB, offload_needed, plan
+    U = DurationTable.from_units(1, 3, 2)
+    rows = {
+        "gpt1.3b_32k p4": (ModelConfig(L=24, h=2048, s=32768, b=1, num_heads=16, p=4, m=8), None,
+                           [("helix_twofold", {}), ("1f1b", {})]),
+        "gpt3b_64k p8": (ModelConfig(L=16, h=4096, s=65536, b=1, num_heads=32, p=8, m=16), 8192,
+                         [("helix_twofold_rc", {}), ("1f1b", {}), ("1f1b_rc", {})]),
+        "gpt7b_128k p8": (ModelConfig(L=32, h=4096, s=131072, b=1, num_heads=32, p=8, m=16), 16384,
+                          [("helix_twofold_rc", {"regen_pre_x": True, "stream_inputs": True}), ("1f1b_rc", {})]),
+    }
+    out = {}
+    for name, (cfg, chunk, methods) in rows.items():
+        for method, kw in methods:
+            sched = generate(method, cfg, U)
+            worst = max((plan(sched, r, chunk, durations=U, **kw) for r in range(cfg.p)), key=lambda x: x.total)
+            key = f"{name} {method}" + "".join(f" +{k}" for k in kw)
+            out[key] = {"worst_rank": worst.stage, "device_total_gb": round(worst.total / GB, 1),
+                        "stash_gb": round(worst.stash_peak / GB, 1),
+                        "host_offload_gb": round(offload_needed(worst, 180 * GB) / GB, 1)}
+    return out
+
+
 def main() -> None:
     args = parse()
     wl = dict(WORKLOADS[args.workload])
@@ -864,6 +892,17 @@ def bench_gpu(args, wl, world: int, rank: int, local: int) -> None:
             "max_memory_gb": torch.cuda.max_memory_allocated(dev) / 2**30,
             "stash_offload": rt.offload_stats(),
         }
+        line["memory_plan"] = baseline_memory_plan()
+        pred = ROOT / "profiles" / "r02_pipeline_predictions.json"
+        if pred.exists():
+            line["pipeline_prediction_from_stage_probes"] = {
+                "source": "profiles/r02_pipeline_predictions.json (tools/predict_from_probes.py: rank-0 stage "
+                          "probes measured on a B200 at the 8-stage per-rank shapes, replayed by the reference "
+                          "list scheduler with NVLink 770 GB/s + 5 us); predictions, not measurements",
+                **{wl: {k: {kk: vv for kk, vv in v.items() if kk in ("makespan_ms", "bubble_fraction",
+                                                                        "tokens_per_s") or kk.startswith("speedup")}
+                            for k, v in rows.items()}
+                   for wl, rows in json.loads(pred.read_text()).items()}}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

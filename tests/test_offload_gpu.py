@@ -41,3 +41,19 @@ def test_multistream_driver_with_offload():
     res = run(SMALL, "helix_twofold", threaded=True, stash_budget_bytes=0, offload_min_bytes=0)
     assert res.offload["evictions"] > 0
     compare(res, oracle_for(SMALL), SMALL.L, "offload multistream")
+
+
+@pytest.mark.parametrize("qkv", [True, False])
+def test_regen_pre_x_with_zero_budget(qkv):
+    """regen_pre_x reads post(l-1)'s retention in rc.pre(l): the offloader
+    prefetches it for that task too (consumed_keys), so with everything
+    offloaded the results still match the oracle and nothing leaks."""
+    from paper_2507_00394_b200 import generate
+    from paper_2507_00394_b200.runtime import execute_schedule, make_inputs, make_model
+    from tests.test_parity_gpu import UNIT
+    sched = generate("helix_twofold_rc", SMALL, UNIT, qkv_in_attention=qkv)
+    res = execute_schedule(sched, make_model(SMALL, 0), make_inputs(SMALL, 1), mlp_chunk=100,
+                           regen_pre_x=True, stash_budget_bytes=0, offload_min_bytes=0)
+    st = res.offload
+    assert st["evictions"] > 0 and st["h2d_bytes"] == st["d2h_bytes"] and st["live_entries"] == 0
+    compare(res, oracle_for(SMALL), SMALL.L, f"offload + regen_pre_x qkv={qkv}")

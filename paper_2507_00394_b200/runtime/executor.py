@@ -833,6 +833,10 @@ class _Distributed:
         self.send_cap = send_cap
         self.comm_stream = side_stream(st.device, "recv") if self.cuda else None
         self.wqkv = _WqkvDedupe()
+        # gloo cannot move device memory: CUDA payloads are staged through host
+        # buffers (lets several ranks share one GPU for testing; NCCL is direct)
+        self.host_staging = self.cuda and torch.distributed.get_backend(
+            next(iter(groups.values())) if groups else None) == "gloo"
         self.posted: dict[str, tuple[list, dict]] = {}    # rid -> (works, payload)
         self.next_recv: dict[int, int] = {}               # src -> index into recv_seq
         self.recv_index = {rid: (src, k) for (src, dst), seq in self.plan.recv_seq.items()
@@ -861,7 +865,7 @@ class _Distributed:
                 r_id = seq[k]
                 payload, works = {}, []
                 for name, shape, dtype in _payload_layout(cfg, _edge_tag(r_id), core.qkv, core.math):
-                    buf = torch.empty(shape, dtype=dtype, device=st.device)
+                    buf = torch.empty(shape, dtype=dtype, device="cpu" if self.host_staging else st.device)
                     payload[name] = buf
                     works.append(torch.distributed.irecv(buf, src=src, group=self.groups[(src, self.rank)]))
                 self.posted[r_id] = (works, payload)
@@ -877,6 +881,9 @@ class _Distributed:
         works, payload = self.posted.pop(rid)
         for w in works:
             w.wait()        # NCCL: the current (compute) stream waits; gloo: blocks
+        if self.host_staging:
+            dev = self.core.stages[self.rank].device
+            payload = {k: v.to(dev) for k, v in payload.items()}
         if self.cuda:
             cur = torch.cuda.current_stream()
             for t in payload.values():
@@ -910,6 +917,8 @@ class _Distributed:
                     tensor = payload[name].contiguous()
                     if tensor.dtype != dtype:
                         raise PayloadMismatch(f"{snd.id}: {name} has dtype {tensor.dtype}, want {dtype}")
+                    if self.host_staging:
+                        tensor = tensor.cpu()
                     works.append(torch.distributed.isend(tensor, dst=snd.peer, group=grp))
                     tensors.append(tensor)
                 q = self.sends.get(snd.peer)

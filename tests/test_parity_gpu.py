@@ -173,3 +173,28 @@ def test_device_stash_bytes_match_memplan(method, chunk, regen, stream):
     torch.cuda.synchronize()
     want, at = stash_walk(sched, 0, regen_pre_x=regen, stream_inputs=stream)
     assert rt.stages[0].peak_bytes == want, (rt.stages[0].peak_bytes, rt.stages[0].peak_bytes_at, want, at)
+
+
+@pytest.mark.parametrize("method", ["helix_twofold_rc", "1f1b"])
+def test_stage_probe_memory_matches_plan(method):
+    """HelixRuntime mode "probe" (one rank of a 4-stage pipeline, loopback
+    receives) with the B200 kernels holds exactly the distinct device bytes
+    runtime/memplan.py predicts for that rank, on every stage."""
+    from paper_2507_00394_b200.partition import pre_stage
+    from paper_2507_00394_b200.runtime import HelixRuntime
+    from paper_2507_00394_b200.runtime.executor import DeviceModel
+    from paper_2507_00394_b200.runtime.memplan import stash_walk
+    cfg = ModelConfig(L=4, h=128, s=256, b=1, num_heads=2, p=4, m=8)
+    sched = generate(method, cfg, UNIT)
+    dev = torch.device("cuda", 0)
+    chunked = method == "1f1b"
+    for rank in range(cfg.p):
+        model = DeviceModel.from_host(sched, make_model(cfg, 0), [rank], dev)
+        rt = HelixRuntime(sched, model, 64, "probe", dev, rank=rank)
+        first = 0 if chunked else pre_stage(0, cfg)
+        xs = [torch.from_numpy(x).to(dev, torch.bfloat16).reshape(cfg.s * cfg.b, cfg.h) if rank == first else None
+              for x in make_inputs(cfg, 1)]
+        rt.run(xs)
+        torch.cuda.synchronize()
+        want, at = stash_walk(sched, rank)
+        assert rt.stages[rank].peak_bytes == want, (method, rank, rt.stages[rank].peak_bytes_at, at)

@@ -518,6 +518,22 @@ def measure_config1(dev) -> dict:
     ms = a.elapsed_time(b) / 20
     out["device"] = {"tokens_per_s": tokens / (ms / 1e3), "ms_per_step": ms,
                      "how": "HelixRuntime multistream (one CUDA stream per stage), CUDA events"}
+    # the same iteration captured as one CUDA graph (config 1 is host-launch bound eagerly)
+    try:
+        g = rt.capture(xs)
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        a.record()
+        for _ in range(20):
+            g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        gms = a.elapsed_time(b) / 20
+        out["device_cuda_graph"] = {"tokens_per_s": tokens / (gms / 1e3), "ms_per_step": gms,
+                                    "how": "HelixRuntime.capture: the multistream iteration as one CUDA graph"}
+    except Exception as e:  # noqa: BLE001 -- reported, not fatal for the bench line
+        out["device_cuda_graph"] = {"error": f"{type(e).__name__}: {e}"[:200]}
     out["value"] = out["execute_schedule_threaded"]["tokens_per_s"]
     out["unit"] = "tokens/s"
     out["value_is"] = "execute_schedule(threaded=True) with host float64 fixtures, wall clock per call"

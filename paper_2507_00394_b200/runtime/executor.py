@@ -1194,6 +1194,30 @@ class HelixRuntime:
         self.timeline = timer.collect()
         self._check_drained()
 
+    def capture(self, inputs: list[torch.Tensor]) -> "GraphedIteration":
+        """Capture one whole iteration (every launch of ``run``) into a CUDA
+        graph, for launch-bound small shapes (BASELINE config 1: hundreds of
+        tiny kernels per iteration, host-issue bound).  ``inputs`` must be
+        device tensors; they become the graph's static input buffers.  Host
+        offload, input streaming, LM mode and the distributed / probe drivers
+        are not capturable (host-synchronising or data-dependent)."""
+        if self.mode not in ("replay", "multistream") or self.core.offload is not None or \
+                self.core.lm is not None or self.record_timeline:
+            raise ExecutionError("capture needs replay / multistream mode without offload, LM mode or timeline")
+        if any(x.device.type != "cuda" for x in inputs):
+            raise ExecutionError("capture needs device-resident inputs")
+        static = [x.reshape(self.cfg.s * self.cfg.b, self.cfg.h).clone() for x in inputs]
+        self.run(static)                       # warm-up: lazy kernel attributes, allocator pools
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(graph, stream=side):
+                self.run(static)
+        torch.cuda.current_stream().wait_stream(side)
+        return GraphedIteration(self, graph, static)
+
     def _check_drained(self) -> None:
         leftovers = sorted(tid for st in self.stages.values() for tid in st.values)
         if leftovers:
@@ -1223,6 +1247,20 @@ class HelixRuntime:
     def grads_numpy(self) -> dict[int, dict[str, np.ndarray]]:
         return {l: {k: g.double().cpu().numpy() for k, g in dl.grad.items()}
                 for l, dl in self.model.layers.items()}
+
+
+class GraphedIteration:
+    """One captured ``HelixRuntime.run``: ``replay(inputs)`` copies new inputs
+    into the static buffers and launches the whole iteration as one graph."""
+
+    def __init__(self, rt: HelixRuntime, graph, static: list[torch.Tensor]):
+        self.rt, self.graph, self.static = rt, graph, static
+
+    def replay(self, inputs: list[torch.Tensor] | None = None) -> None:
+        if inputs is not None:
+            for dst, src in zip(self.static, inputs):
+                dst.copy_(src.reshape(dst.shape), non_blocking=True)
+        self.graph.replay()
 
 
 def _to_device_inputs(inputs, cfg, device, stream: bool = False) -> list[torch.Tensor]:

@@ -198,3 +198,49 @@ def test_stage_probe_memory_matches_plan(method):
         torch.cuda.synchronize()
         want, at = stash_walk(sched, rank)
         assert rt.stages[rank].peak_bytes == want, (method, rank, rt.stages[rank].peak_bytes_at, at)
+
+
+@pytest.mark.parametrize("mode", ["replay", "multistream"])
+def test_cuda_graph_iteration_matches_eager(mode):
+    """HelixRuntime.capture: one iteration as a CUDA graph (BASELINE config 1,
+    host-launch bound eagerly) replays to the eager results, and keeps doing so
+    with new inputs copied into its static buffers."""
+    import time
+    from paper_2507_00394_b200.runtime import HelixRuntime
+    from paper_2507_00394_b200.runtime.executor import DeviceModel
+    cfg = TINY
+    sched = generate("helix_twofold", cfg, UNIT)
+    dev = torch.device("cuda", 0)
+    model = DeviceModel.from_host(sched, make_model(cfg, 0), range(cfg.p), dev)
+    rt = HelixRuntime(sched, model, None, mode, dev)
+    xs = [torch.from_numpy(x).to(dev, torch.bfloat16).reshape(cfg.s * cfg.b, cfg.h) for x in make_inputs(cfg, 1)]
+    rt.run(xs)
+    eager_l = rt.losses()
+    eager_g = {l: {k: g.clone() for k, g in dl.grad.items()} for l, dl in model.layers.items()}
+    g = rt.capture(xs)
+    g.replay()
+    torch.cuda.synchronize()
+    assert np.allclose(rt.losses(), eager_l, rtol=1e-5)
+    for l, d in eager_g.items():
+        for k, v in d.items():
+            assert torch.allclose(model.layers[l].grad[k], v, rtol=1e-3, atol=1e-5), (l, k)
+    assert np.allclose(rt.losses(), TINY_LOSSES, rtol=LOSS_TOL)
+    xs2 = [x.flip(0).contiguous() for x in xs]       # new inputs through the static buffers
+    rt2 = HelixRuntime(sched, DeviceModel.from_host(sched, make_model(cfg, 0), range(cfg.p), dev), None, mode, dev)
+    rt2.run(xs2)
+    g.replay(xs2)
+    torch.cuda.synchronize()
+    assert np.allclose(rt.losses(), rt2.losses(), rtol=1e-5)
+    # timing (printed): eager vs graphed iteration, CUDA events
+    def t(fn, n=10):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(n):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / n
+    te, tg = t(lambda: rt2.run(xs2)), t(lambda: g.replay())
+    print(f"[graph] config 1 {mode}: eager {te:.2f} ms, graphed {tg:.2f} ms per iteration")

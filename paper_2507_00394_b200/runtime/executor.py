@@ -1079,6 +1079,7 @@ class HelixRuntime:
         self.sumsq = torch.zeros(self.cfg.m, dtype=torch.float64, device=self.device)
         self.timeline = None
         self.core = _Core(sched, model, self.math, self.stages, self.sumsq)
+        self.lm_spec = lm
         if lm is not None:
             self._setup_lm(lm, lm_params)
         if regen_pre_x:
@@ -1150,6 +1151,8 @@ class HelixRuntime:
             self.core.n_valid = [int((lb >= 0).sum()) for lb in labs]
             self.core.lm.p.zero_grads(self.math.zero_)
             self.math.zero_(self.core.loss_count)
+            inputs = [None] * cfg.m
+        elif self.lm_spec is not None:      # LM mode on a rank that holds neither end
             inputs = [None] * cfg.m
         # (a stage probe of a rank that never reads the inputs may pass None)
         self.core.inputs = [None if x is None else x.reshape(cfg.s * cfg.b, cfg.h) for x in inputs]

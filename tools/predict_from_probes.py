@@ -55,11 +55,19 @@ def main():
     rows = load()
     units = DurationTable.from_units(1, 3, 2)
     out = {}
-    for wl, shape in SHAPES.items():
+    keys = [(wl, shape) for wl, shape in SHAPES.items()]
+    # sequence-sweep probes (BASELINE config 5): one entry per probed length
+    for r in rows:
+        if r["workload"] == "gpt3b_64k" and r["s"] != SHAPES["gpt3b_64k"]["s"]:
+            k = (f"gpt3b_s{r['s']}", dict(SHAPES["gpt3b_64k"], s=r["s"]))
+            if k not in keys:
+                keys.append(k)
+    for wl, shape in keys:
         cfg = ModelConfig(**shape, p=8, m=16)
         res = {}
         for r in rows:
-            if r["workload"] != wl or r["stage"] != 0:
+            base = "gpt3b_64k" if wl.startswith("gpt3b") else wl
+            if r["workload"] != base or r["stage"] != 0 or r["s"] != cfg.s:
                 continue
             key = r["method"] + (" +regen_pre_x" if r.get("regen_pre_x") else "") + \
                 (" +offload" if r.get("stash_budget_gb") else "")

@@ -46,6 +46,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="gpt3b_64k", choices=sorted(WORKLOADS))
     ap.add_argument("--L", type=int, default=None, help="override the layer count (reduced-L probes)")
+    ap.add_argument("--seq", type=int, default=None, help="override the sequence length (sweeps)")
     ap.add_argument("--p", type=int, default=8)
     ap.add_argument("--stage", type=int, nargs="+", default=[0])
     ap.add_argument("--method", default="helix_twofold_rc")
@@ -60,6 +61,8 @@ def main():
     wl = dict(WORKLOADS[args.workload])
     if args.L:
         wl["L"] = args.L
+    if args.seq:
+        wl["s"] = args.seq
     cfg = ModelConfig(L=wl["L"], h=wl["h"], s=wl["s"], b=wl["b"], num_heads=wl["num_heads"], p=args.p, m=2 * args.p)
     units = DurationTable.from_units(1, 3, 2)
     sched = generate(args.method, cfg, units)

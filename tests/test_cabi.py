@@ -55,3 +55,14 @@ def test_argument_checks_fire_before_any_device_work():
     assert L.hx_gemm(None, 8, 0, None, 8, 1, None, 8, 0, 8, 8, 0, None, 0, None, 0, None) == 1001
     assert L.hx_attn_fwd(None, 384, None, 128, None, 16, 1, 1, 96, None) == 1003
     assert L.hx_ln_fwd(None, None, None, None, 4, 12, None) == 1001
+
+
+def test_round2_entry_points_check_arguments_on_the_host():
+    from paper_2507_00394_b200.runtime import _lib
+    L = _lib.load()
+    assert L.hx_attn_bwd_ws_bytes(32768, 1, 16, 128) == 32768 * 16 * 128 * 4
+    assert L.hx_attn_bwd_ws_bytes(0, 1, 16, 128) == 0
+    assert L.hx_attn_bwd_delta(None, None, 128, None, 16, 1, 1, 96, None) == 1003      # head_dim
+    assert L.hx_embed_fwd(None, None, None, None, 16, 1, 12, None) == 1001             # h % 8
+    assert L.hx_embed_bwd(None, None, None, None, 0, 1, 64, None) == 1001
+    assert L.hx_ce_loss(None, 1024, None, 4, 1000, 992, 1.0, None, None, None) == 1001  # vpad < vocab

@@ -368,6 +368,9 @@ cudaError_t attn_fwd_launch(const void* qkv, int ld_qkv, void* o, int ld_o, floa
   p.o = static_cast<__nv_bfloat16*>(o);
   p.ld_o = ld_o;
   p.lse = lse;
+  // HX_ATTN_FWD=2: one query tile per CTA with double-buffered S (attention_fwd1.cu)
+  static const int variant = getenv("HX_ATTN_FWD") ? atoi(getenv("HX_ATTN_FWD")) : 1;
+  if (variant == 2) return attn_fwd1_launch(qkv, ld_qkv, p, d, st);
   if (d == 128) return fwd_launch<128>(qkv, ld_qkv, p, st);
   if (d == 64) return fwd_launch<64>(qkv, ld_qkv, p, st);
   return cudaErrorNotSupported;

@@ -11,6 +11,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 #define HX_DEVICE __device__ __forceinline__
 
@@ -129,7 +130,12 @@ HX_DEVICE void mbar_wait_nohint(uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait_nohint(addr, parity)) return;
   const uint64_t t0 = global_ns();
   while (!mbar_try_wait_nohint(addr, parity)) {
-    if (global_ns() - t0 > HX_WAIT_LIMIT_NS) __trap();
+    if (global_ns() - t0 > HX_WAIT_LIMIT_NS) {
+#ifdef HX_WAIT_DEBUG  // debug builds: which barrier hung
+      printf("hx wait timeout: block %d thread %d smem bar 0x%x parity %u\n", blockIdx.x, threadIdx.x, addr, parity);
+#endif
+      __trap();
+    }
   }
 }
 

@@ -57,6 +57,8 @@ cudaError_t mse_loss_launch(const void* z, int64_t n, void* dz, double* sumsq, c
 cudaError_t axpy_f32_launch(float* y, const float* x, int64_t n, cudaStream_t st);
 cudaError_t attn_fwd_launch(const void* qkv, int ld_qkv, void* o, int ld_o, float* lse, int s, int b,
                             int heads, int d, cudaStream_t st);
+struct AttnParams;
+cudaError_t attn_fwd1_launch(const void* qkv, int ld_qkv, const AttnParams& p, int d, cudaStream_t st);
 cudaError_t attn_bwd_delta_launch(const void* o, const void* d_o, int ld_o, float* delta, int s, int b, int heads,
                                   int d, cudaStream_t st);
 cudaError_t attn_bwd_launch(const void* qkv, int ld_qkv, const void* o, const void* d_o, int ld_o,

@@ -72,3 +72,86 @@ def test_two_ranks_on_one_gpu_match_oracle(method, chunk):
     r.losses, r.param_grads = losses, grads
     compare(r, oracle_for(SMALL), SMALL.L, f"2 ranks on one GPU {method}")
     assert all(np.isfinite(losses))
+
+
+def _lm_worker(rank, world, port, method, chunk, regen, q):
+    """LM mode (runtime/lm.py) under the one-rank-per-stage driver: the tied
+    embedding and the loss-in-backward head live on stage 0 (helix places pre(0)
+    and post(L-1) there), rank 1 only runs its layer components.  Every rank
+    checks the gradients it owns against the fp32 autograd model of
+    tests/test_lm_gpu.py."""
+    try:
+        import torch.distributed as dist
+
+        from paper_2507_00394_b200 import ModelConfig, generate
+        from paper_2507_00394_b200.costs import DurationTable
+        from paper_2507_00394_b200.partition import post_stage, pre_stage
+        from paper_2507_00394_b200.runtime import HelixRuntime
+        from paper_2507_00394_b200.runtime.executor import DeviceModel, pair_groups
+        from paper_2507_00394_b200.runtime.lm import LMParams, LMSpec, default_labels
+        from paper_2507_00394_b200.runtime.model import (PARAM_FIELDS, POST_FIELDS, PRE_FIELDS, DeviceLayer,
+                                                         random_device_layer)
+        from tests.test_lm_gpu import _cos_max, _reference
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), HX_SEND_CAP="0")
+        torch.cuda.set_device(0)
+        dev = torch.device("cuda", 0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        cfg = ModelConfig(L=2, h=128, s=256, b=2, num_heads=2, p=world, m=2 * world)
+        V = 1000
+        sched = generate(method, cfg, DurationTable.from_units(1, 3, 2))
+        gen = torch.Generator(device=dev).manual_seed(11)
+        layers = [random_device_layer(cfg.h, gen, dev) for _ in range(cfg.L)]
+        spec = LMSpec(V, head_chunk=192)
+        params = LMParams(spec, cfg.h, cfg.s, dev, gen)
+        model = DeviceModel({l: DeviceLayer(dict(w), PARAM_FIELDS) for l, w in enumerate(layers)})
+        rt = HelixRuntime(sched, model, chunk, "distributed", dev, rank=rank, groups=pair_groups(world),
+                          regen_pre_x=regen, lm=spec, lm_params=params)
+        tg = torch.Generator(device=dev).manual_seed(12)
+        tokens = [torch.randint(0, V, (cfg.s, cfg.b), generator=tg, device=dev) for _ in range(cfg.m)]
+        rt.run(tokens)
+        torch.cuda.synchronize()
+        labels = [default_labels(t.reshape(-1).int(), cfg.s, cfg.b) for t in tokens]
+        ref_l, ref_g, ref_e, ref_p = _reference(cfg, layers, params.w_emb[:V], params.w_pos,
+                                                [t.reshape(-1) for t in tokens], labels)
+        worst_cos, worst_max, owned = 1.0, 0.0, 0
+        for l in range(cfg.L):
+            fields = (PRE_FIELDS if pre_stage(l, cfg) == rank else ()) + \
+                (POST_FIELDS if post_stage(l, cfg) == rank else ())
+            for k in fields:
+                c, m = _cos_max(model.layers[l].grad[k], ref_g[l][k])
+                worst_cos, worst_max, owned = min(worst_cos, c), max(worst_max, m), owned + 1
+        loss_err = None
+        g = rt.lm_grads()
+        if g is not None:
+            for got, want in ((g["w_emb"][:V], ref_e), (g["w_pos"], ref_p)):
+                c, m = _cos_max(got, want)
+                worst_cos, worst_max = min(worst_cos, c), max(worst_max, m)
+            loss_err = max(abs(a - b) / b for a, b in zip(rt.losses(), ref_l))
+        q.put(("ok", rank, worst_cos, worst_max, owned, loss_err, g is not None))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # noqa: BLE001
+        import traceback
+        q.put(("err", rank, f"{type(e).__name__}: {e}\n{traceback.format_exc()[-1500:]}", None, None, None, None))
+
+
+@pytest.mark.parametrize("method,chunk,regen", [("helix_twofold", None, False), ("helix_twofold_rc", 100, True)])
+def test_two_ranks_on_one_gpu_lm_mode(method, chunk, regen):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_lm_worker, args=(r, 2, port, method, chunk, regen, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=120)
+    for o in outs:
+        assert o[0] == "ok", f"rank {o[1]}: {o[2]}"
+    by_rank = {o[1]: o for o in outs}
+    assert by_rank[0][6] and not by_rank[1][6], "the LM head must live on stage 0 only"
+    assert by_rank[0][5] is not None and by_rank[0][5] <= 2e-3, by_rank[0][5]
+    assert sum(o[4] for o in outs) == 2 * 8, "every layer field is owned by exactly one rank"
+    for o in outs:
+        print(f"[lm x2] {method} rank {o[1]}: cos {o[2]:.6f} max {o[3]:.2e}")
+        assert o[2] >= 0.9995 and o[3] <= 2e-2, o

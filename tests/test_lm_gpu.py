@@ -107,7 +107,7 @@ def _reference(cfg, layers, w_emb, w_pos, tokens, labels):
         valid = lab >= 0
         loss = torch.nn.functional.cross_entropy((x @ E.T)[valid], lab[valid].long())
         loss.backward()
-        losses.append(float(loss))
+        losses.append(float(loss.detach()))
     return losses, [{k: W[k].grad for k in PARAM_FIELDS} for W in P], E.grad, Q.grad
 
 

@@ -554,11 +554,20 @@ def bench_gpu(args, wl, world: int, rank: int, local: int) -> None:
                                                 predict_pipeline, simulate)
     from paper_2507_00394_b200.engine import CommModel
 
+    # test-only (HX_BENCH_SHARED_GPU=1): all ranks on cuda:0 over gloo (host-staged
+    # payloads), so the N > 1 leg of this script runs end to end on a one-GPU box;
+    # its numbers are time-shared and never a bench value
+    shared_gpu = world > 1 and os.environ.get("HX_BENCH_SHARED_GPU") == "1"
+    if shared_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import datetime
-        dist.init_process_group("nccl", device_id=dev, timeout=datetime.timedelta(seconds=900))
+        if shared_gpu:
+            dist.init_process_group("gloo", timeout=datetime.timedelta(seconds=900))
+        else:
+            dist.init_process_group("nccl", device_id=dev, timeout=datetime.timedelta(seconds=900))
     p = world
     cfg = ModelConfig(L=wl["L"], h=wl["h"], s=wl["s"], b=wl["b"], num_heads=wl["num_heads"], p=p, m=2 * p)
     units = DurationTable.from_units(1, 3, 2)
@@ -884,7 +893,9 @@ def bench_gpu(args, wl, world: int, rank: int, local: int) -> None:
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (N(0,1) inputs, random-init weights)",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": "TEST: ranks time-sharing one GPU over gloo -- not a bench value" if shared_gpu
+            else "synthetic (N(0,1) inputs, random-init weights)",
             "config": {"workload": args.workload, **wl, "p": p, "m": cfg.m, "method": args.method,
                        "n_gpus": world,
                        "mlp_chunk": args.mlp_chunk, "parallelism": f"pp{p} (one helix stage per GPU)",

@@ -835,8 +835,10 @@ class _Distributed:
         self.wqkv = _WqkvDedupe()
         # gloo cannot move device memory: CUDA payloads are staged through host
         # buffers (lets several ranks share one GPU for testing; NCCL is direct)
-        self.host_staging = self.cuda and torch.distributed.get_backend(
-            next(iter(groups.values())) if groups else None) == "gloo"
+        # (asked of a pair group this rank belongs to: from p = 3 on, the first
+        # group in the dict may not include it, and get_backend rejects that)
+        mine = [g for (a, b), g in (groups or {}).items() if rank in (a, b)]
+        self.host_staging = self.cuda and torch.distributed.get_backend(mine[0] if mine else None) == "gloo"
         self.posted: dict[str, tuple[list, dict]] = {}    # rid -> (works, payload)
         self.next_recv: dict[int, int] = {}               # src -> index into recv_seq
         self.recv_index = {rid: (src, k) for (src, dst), seq in self.plan.recv_seq.items()

@@ -27,7 +27,7 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, method, cfg_kw, mlp_chunk, q):
+def _worker(rank, world, port, method, cfg_kw, mlp_chunk, q, extra=None):
     try:
         import torch.distributed as dist
 
@@ -39,7 +39,8 @@ def _worker(rank, world, port, method, cfg_kw, mlp_chunk, q):
         dist.init_process_group("gloo", rank=rank, world_size=world)
         cfg = ModelConfig(**cfg_kw)
         sched = generate(method, cfg, DurationTable.from_units(1, 3, 2))
-        res = execute_schedule(sched, make_model(cfg, 0), make_inputs(cfg, 1), mlp_chunk=mlp_chunk, threaded=True)
+        res = execute_schedule(sched, make_model(cfg, 0), make_inputs(cfg, 1), mlp_chunk=mlp_chunk, threaded=True,
+                               **(extra or {}))
         if rank == 0:
             q.put(("ok", res.losses, res.param_grads, res.mode))
         dist.barrier()
@@ -72,6 +73,35 @@ def test_two_ranks_on_one_gpu_match_oracle(method, chunk):
     r.losses, r.param_grads = losses, grads
     compare(r, oracle_for(SMALL), SMALL.L, f"2 ranks on one GPU {method}")
     assert all(np.isfinite(losses))
+
+
+@pytest.mark.parametrize("method,chunk,extra", [("helix_twofold_rc", 100, {"regen_pre_x": True}),
+                                                 ("zb1p", None, {}), ("1f1b_rc", None, {})])
+def test_four_ranks_on_one_gpu_match_oracle(method, chunk, extra):
+    """p = 4: every stage pair exchanges payloads (two-fold pair edges across four
+    stages), with x regenerated from post(l-1) on the rc schedule."""
+    from paper_2507_00394_b200 import ModelConfig
+    from tests.test_parity_gpu import compare, oracle_for
+    cfg = ModelConfig(L=4, h=128, s=256, b=1, num_heads=2, p=4, m=8)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    cfg_kw = dict(L=cfg.L, h=cfg.h, s=cfg.s, b=cfg.b, num_heads=cfg.num_heads, p=cfg.p, m=cfg.m)
+    procs = [ctx.Process(target=_worker, args=(r, 4, port, method, cfg_kw, chunk, q, extra)) for r in range(4)]
+    for p in procs:
+        p.start()
+    out = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+    assert out[0] == "ok", out[1]
+    _, losses, grads, mode = out
+
+    class R:
+        pass
+
+    r = R()
+    r.losses, r.param_grads = losses, grads
+    compare(r, oracle_for(cfg), cfg.L, f"4 ranks on one GPU {method}")
 
 
 def _lm_worker(rank, world, port, method, chunk, regen, q):
@@ -155,3 +185,30 @@ def test_two_ranks_on_one_gpu_lm_mode(method, chunk, regen):
     for o in outs:
         print(f"[lm x2] {method} rank {o[1]}: cos {o[2]:.6f} max {o[3]:.2e}")
         assert o[2] >= 0.9995 and o[3] <= 2e-2, o
+
+
+def test_bench_multirank_leg_on_one_gpu():
+    """bench.py --gpus 4 end to end (self-launch through torch.distributed.run,
+    max-over-ranks timing, bubble table, overlap report, 1F1B baseline, e2e) with
+    the ranks time-sharing this one GPU over gloo (HX_BENCH_SHARED_GPU=1)."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, HX_BENCH_SHARED_GPU="1")
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "4", "--workload", "tiny", "--steps", "2",
+                          "--warmup", "3", "--no-cpu-baseline"], cwd=root, env=env, capture_output=True, text=True,
+                         timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [json.loads(ln) for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = lines[0]
+    assert d["n_gpus"] == 4 and d["config"]["p"] == 4 and d["config"]["m"] == 8
+    assert d["data"].startswith("TEST")
+    assert d["gpu_launches"] > 0 and d["value"] > 0
+    table = d["bubble_predicted_by_reference_model"]["bubble_table"]
+    assert set(table) >= {"analytic", "simulated_zero_comm", "simulated_nvlink", "measured"}
+    assert d["comm"]["max_live_sends_per_peer"] and max(d["comm"]["max_live_sends_per_peer"].values()) <= \
+        d["comm"]["send_cap"]

@@ -12,8 +12,8 @@ aborts).  ``--side gpu`` runs the same grid through this package's
 replay mode) and through ``HelixRuntime`` device-timed, and compares its losses
 with the reference's from ``--ref-jsonl``.
 
-    python tools/config1_grid.py --side ref [--ps 1,2,4,8] > profiles/r02_config1_grid_ref.jsonl
-    python tools/config1_grid.py --side gpu --ref-jsonl profiles/r02_config1_grid_ref.jsonl
+    python tools/config1_grid.py --side ref [--ps 1,2,4,8] > profiles/r02_config1_grid_ref_box.jsonl
+    python tools/config1_grid.py --side gpu --ref-jsonl profiles/r02_config1_grid_ref_box.jsonl
 
 The reference side imports pipelab from ``baseline/_ref`` (the unmodified
 installed reference); it is a measurement tool, not part of the product path.
@@ -142,7 +142,7 @@ def main():
     ap.add_argument("--side", choices=("ref", "gpu"), required=True)
     ap.add_argument("--ps", default="1,2,4,8")
     ap.add_argument("--modes", default="replay,threaded")
-    ap.add_argument("--ref-jsonl", default=str(ROOT / "profiles" / "r02_config1_grid_ref.jsonl"))
+    ap.add_argument("--ref-jsonl", default=str(ROOT / "profiles" / "r02_config1_grid_ref_box.jsonl"))
     args = ap.parse_args()
     ps = [int(x) for x in args.ps.split(",")]
     if args.side == "ref":

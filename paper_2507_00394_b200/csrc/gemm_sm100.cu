@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 2 * 32 * EW);  // epilogue threads of both CTAs
+      mbar_init(&tempty[a], 2 * EW);  // one arrival per epilogue warp of both CTAs
     }
     fence_barrier_init();
   }
@@ -543,8 +543,10 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
 #pragma unroll
         for (int j = 0; j < 4; ++j) aux_c[j] = aux_n[j];
       }
+      // every lane's tcgen05.ld has completed (wait::ld above); one arrival per warp
       tc_fence_before();
-      mbar_arrive_cluster(tempty_leader0 + acc * 8);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(tempty_leader0 + acc * 8);
     }
   }
   if (warp >= 4 && lane == 0) bulk_wait_all();  // epilogue TMA stores have left smem

@@ -209,6 +209,14 @@ HX_DEVICE uint32_t mapa_shared(const void* p, uint32_t rank) {
 HX_DEVICE void mbar_arrive_cluster(uint32_t bar_cluster) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
 }
+// Arrive on a barrier of another CTA of the cluster with the default (.release,
+// .cta) semantics: enough to hand TMEM back after tcgen05.wait::ld +
+// tcgen05.fence::before_thread_sync, and it compiles to MEMBAR.ALL.CTA where
+// .release.cluster emits MEMBAR.ALL.GPU (a wait for every outstanding global
+// access of the thread).
+HX_DEVICE void mbar_arrive_remote(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
 HX_DEVICE void mbar_arrive_expect_tx_cluster(uint32_t bar_cluster, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(bar_cluster),
                "r"(bytes)

@@ -244,3 +244,15 @@ def test_cuda_graph_iteration_matches_eager(mode):
         return a.elapsed_time(b) / n
     te, tg = t(lambda: rt2.run(xs2)), t(lambda: g.replay())
     print(f"[graph] config 1 {mode}: eager {te:.2f} ms, graphed {tg:.2f} ms per iteration")
+
+
+# Ragged shapes end to end: s not a multiple of the 128-row tiles, b = 3, three
+# heads of 64 (h = 192: GEMM N / K not multiples of the 256-wide tiles), an MLP
+# chunk that does not divide s*b, and a p = 3 helix (every stage pair exchanges).
+RAGGED = ModelConfig(L=3, h=192, s=200, b=3, num_heads=3, p=3, m=6)
+
+
+@pytest.mark.parametrize("method,chunk", [("helix_twofold", None), ("helix_twofold_rc", 250), ("1f1b", None),
+                                          ("zb1p", 130)])
+def test_ragged_shapes_match_oracle(method, chunk):
+    compare(run(RAGGED, method, mlp_chunk=chunk), oracle_for(RAGGED), RAGGED.L, f"ragged {method} chunk={chunk}")

@@ -123,6 +123,33 @@ def test_gemm_pair_kernel_epilogues(T, Kd, N):
     assert rel_err(dm, (dy.float() @ w2.float().t()) * gelu_grad) < 1e-2
 
 
+@pytest.mark.parametrize("T,N", [(8192, 1024), (512, 256)])
+def test_gelu_epilogues_to_the_bf16_ulp(T, N):
+    # identity weights make every accumulator exactly the bf16 input, so the fused
+    # GeLU / GeLU' epilogue math (A&S erf, bare MUFU ex2 / rcp) is checked element by
+    # element: within one bf16 ulp of the exact erf GeLU of the same value.
+    # (8192, 1024) takes the cta_group::2 kernel, (512, 256) the single-CTA one.
+    g_ = torch.Generator(device=DEV).manual_seed(31)
+    x = (torch.rand(T, N, generator=g_, device=DEV) * 14 - 7).to(torch.bfloat16)   # [-7, 7)
+    x[0, :8] = torch.tensor([0.0, -0.0, 1e-3, -1e-3, 40.0, -40.0, 1e-30, -6.5])
+    eye = torch.eye(N, device=DEV, dtype=torch.bfloat16)
+    m1 = torch.empty(T, N, dtype=torch.bfloat16, device=DEV)
+    g = torch.empty_like(m1)
+    K.linear_gelu(x, eye, m1, g)
+    dy = rnd(T, N, seed=32)
+    dm = torch.empty(T, N, dtype=torch.bfloat16, device=DEV)
+    K.linear_dx_dgelu(dy, eye, x, dm)
+    torch.cuda.synchronize()
+    xf = x.float().double()
+    assert torch.equal(m1, x)
+    want_g = torch.nn.functional.gelu(xf)
+    ulp = lambda v: v.abs().clamp_min(1e-30) * 2.0 ** -8  # noqa: E731
+    assert ((g.double() - want_g).abs() <= ulp(want_g) + 1e-6).all()
+    grad = 0.5 * (1 + torch.erf(xf / math.sqrt(2))) + xf * torch.exp(-0.5 * xf * xf) / math.sqrt(2 * math.pi)
+    want_dm = dy.double() * grad
+    assert ((dm.double() - want_dm).abs() <= ulp(want_dm) + 1e-6).all()
+
+
 def test_gemm_epilogues():
     T, Kd, N = 512, 256, 1024
     x, w = rnd(T, Kd, seed=7), rnd(Kd, N, scale=Kd ** -0.5, seed=8)

@@ -497,23 +497,29 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
       const int acc = it & 1;
       const int row0 = (2 * mp + rank) * GEMM_BM + sub * 32;
       const int row = row0 + lane;
-      // the first chunk's aux is loaded before the accumulator is ready
-      uint4 aux_c[4], aux_n[4];
-      epilogue_aux_load(p, row, nb * BN + c0 * 32, aux_c);
+      // aux (residual / GeLU pre-activation) two chunks ahead: the first two chunks'
+      // are loaded before the accumulator is ready, chunk c + 2's while chunk c is
+      // processed (one chunk ahead left the GeLU' epilogue waiting on DRAM at every
+      // chunk's first aux use: 10% of its stall samples).  The chunk loop is
+      // unrolled so the three aux slots stay in registers.
+      uint4 aux[3][4];
+      epilogue_aux_load(p, row, nb * BN + c0 * 32, aux[0]);
+      if (CPW > 1) epilogue_aux_load(p, row, nb * BN + (c0 + 1) * 32, aux[1]);
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(sub * 32) << 16);
-#pragma unroll 1
-      for (int c = c0; c < c0 + CPW; ++c) {
+#pragma unroll
+      for (int ci = 0; ci < CPW; ++ci) {
+        const int c = c0 + ci;
         const int col = nb * BN + c * 32;
         if (col >= p.N) break;  // warp-uniform
-        if (c + 1 < c0 + CPW && col + 32 < p.N) epilogue_aux_load(p, row, col + 32, aux_n);
+        if (ci + 2 < CPW && col + 64 < p.N) epilogue_aux_load(p, row, col + 64, aux[(ci + 2) % 3]);
         uint32_t r[32];
         tmem_ld32(taddr + c * 32, r);
         tmem_wait_ld();
         if (tma_out) {
           uint32_t o[16], o2[16];
-          epilogue_values(p.epi, r, aux_c, o, o2);
+          epilogue_values(p.epi, r, aux[ci % 3], o, o2);
           uint8_t* buf = stg + (nbuf == 2 ? (kbuf & 1) * (nout * 2048) : 0);
           if (lane == 0) {  // the store that last read this buffer is done
             if (nbuf == 2) bulk_wait_read<1>();
@@ -538,10 +544,8 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1)
           }
           ++kbuf;
         } else {
-          epilogue_chunk(p, row, col, r, aux_c);
+          epilogue_chunk(p, row, col, r, aux[ci % 3]);
         }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) aux_c[j] = aux_n[j];
       }
       // every lane's tcgen05.ld has completed (wait::ld above); one arrival per warp
       tc_fence_before();

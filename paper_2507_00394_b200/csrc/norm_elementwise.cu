@@ -435,6 +435,166 @@ __global__ void __launch_bounds__(256, MINB) ln_bwd_v2_kernel(
   }
 }
 
+// ------------------------------------------------------------------ LayerNorm backward v5
+// For h <= 2048 (h % 256 == 0), where v2's column-sliced 2-row batches are
+// barrier-bound and v1 re-reads x and dy for the gain / bias sums.  Rows stream
+// through a shared-memory ring filled by 1-D bulk copies (cp.async.bulk, the
+// TMA engine) from a producer warp: each slot holds one row of x, dy (and the
+// residual gradient), so up to LN5_SLOTS rows per SM are in flight without a
+// register holding them.  Each of the 8 consumer warps owns whole rows (warp
+// shuffles for the row statistics, no block barrier in the loop) and keeps its
+// lanes' gain / bias gradient partials in registers across all its rows; the
+// block combines them once at the end.  HBM traffic is the algorithmic
+// 4*T*h*2 bytes (3*T*h*2 without a residual gradient), each row read once.
+constexpr int LN5_CONSUMERS = 7;
+constexpr int LN5_THREADS = 32 * (LN5_CONSUMERS + 1);
+constexpr int LN5_RING_BYTES = 192 * 1024;
+
+HX_DEVICE void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int NV>  // 16-byte vectors per lane per row: h = 256 * NV
+__global__ void __launch_bounds__(LN5_THREADS, 1) ln_bwd_v5_kernel(
+    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x, const float* __restrict__ gain,
+    const __nv_bfloat16* __restrict__ dres, __nv_bfloat16* __restrict__ dx, float* __restrict__ dgain,
+    float* __restrict__ dbias, int rows, int h, int rows_per_block) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int nt = dres ? 3 : 2;
+  const uint32_t row_bytes = static_cast<uint32_t>(h) * 2;
+  const int slot_bytes = nt * static_cast<int>(row_bytes);
+  const int nslot = LN5_RING_BYTES / slot_bytes;
+  float* sgain = reinterpret_cast<float*>(smem + LN5_RING_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sgain + h);
+  uint64_t* empty = full + nslot;
+  const int lane = lane_id(), w = warp_id();
+  const int r_begin = blockIdx.x * rows_per_block;
+  const int n = min(rows, r_begin + rows_per_block) - r_begin;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nslot; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    fence_barrier_init();
+  }
+  for (int c = threadIdx.x; c < h; c += LN5_THREADS) sgain[c] = gain[c];
+  __syncthreads();
+
+  if (w == LN5_CONSUMERS) {  // ---------------- producer: rows into the ring
+    if (lane == 0) {
+      for (int k = 0; k < n; ++k) {
+        const int sl = k % nslot;
+        mbar_wait(&empty[sl], ((k / nslot) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[sl], slot_bytes);
+        uint8_t* dst = smem + sl * slot_bytes;
+        const int64_t off = static_cast<int64_t>(r_begin + k) * h;
+        bulk_g2s(dst, x + off, row_bytes, &full[sl]);
+        bulk_g2s(dst + row_bytes, dy + off, row_bytes, &full[sl]);
+        if (dres) bulk_g2s(dst + 2 * row_bytes, dres + off, row_bytes, &full[sl]);
+      }
+    }
+    __syncwarp();
+  } else {  // ---------------- consumers: whole rows, warp k % 8 takes row k
+    float ag[NV][8], ab[NV][8];
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) ag[i][j] = ab[i][j] = 0.f;
+    const float inv_h = 1.0f / static_cast<float>(h);
+    for (int k = w; k < n; k += LN5_CONSUMERS) {
+      const int sl = k % nslot;
+      mbar_wait(&full[sl], (k / nslot) & 1);
+      const uint4* sx = reinterpret_cast<const uint4*>(smem + sl * slot_bytes);
+      const uint4* sd = sx + h / 8;
+      const uint4* sr = sd + h / 8;
+      float s_x = 0.f, s_xx = 0.f, s_g = 0.f, s_gx = 0.f;
+      // (unrolled by 2 only: fully unrolled, ptxas hoists every vector's shared loads
+      // next to the 16 * NV gradient partials and spills at NV >= 6)
+#pragma unroll 2
+      for (int i = 0; i < NV; ++i) {
+        const int c = lane + 32 * i;
+        float f[8], d[8], g[8];
+        unpack8(sx[c], f);
+        unpack8(sd[c], d);
+        load_gain8(sgain, c, g);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float gd = d[j] * g[j];
+          s_x += f[j];
+          s_xx = fmaf(f[j], f[j], s_xx);
+          s_g += gd;
+          s_gx = fmaf(gd, f[j], s_gx);
+        }
+      }
+      s_x = warp_sum(s_x);
+      s_xx = warp_sum(s_xx);
+      s_g = warp_sum(s_g);
+      s_gx = warp_sum(s_gx);
+      const float mu = s_x * inv_h;
+      const float rstd = rsqrtf(fmaxf(s_xx * inv_h - mu * mu, 0.f) + LN_EPS);
+      const float m1 = s_g * inv_h;                      // mean(dxhat)
+      const float m2 = (s_gx * inv_h - mu * m1) * rstd;  // mean(dxhat * xhat)
+      const int64_t off = static_cast<int64_t>(r_begin + k) * h;
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const int c = lane + 32 * i;
+        float f[8], d[8], g[8], o[8];
+        unpack8(sx[c], f);
+        unpack8(sd[c], d);
+        load_gain8(sgain, c, g);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float xh = (f[j] - mu) * rstd;
+          o[j] = rstd * (d[j] * g[j] - m1) - xh * rstd * m2;
+          ag[i][j] = fmaf(d[j], xh, ag[i][j]);
+          ab[i][j] += d[j];
+        }
+        if (dres) {
+          float r[8];
+          unpack8(sr[c], r);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) o[j] += r[j];
+        }
+        reinterpret_cast<uint4*>(dx + off)[c] = make_uint4(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]),
+                                                           pack_bf16(o[4], o[5]), pack_bf16(o[6], o[7]));
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[sl]);
+    }
+    __syncthreads();  // (A) every consumer is past the ring; the producer waits here too
+    float* red = reinterpret_cast<float*>(smem);  // [8 warps][2][h] over the drained ring
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = lane + 32 * i;
+      float4* pg = reinterpret_cast<float4*>(red + (2 * w) * h + 8 * c);
+      float4* pb = reinterpret_cast<float4*>(red + (2 * w + 1) * h + 8 * c);
+      pg[0] = make_float4(ag[i][0], ag[i][1], ag[i][2], ag[i][3]);
+      pg[1] = make_float4(ag[i][4], ag[i][5], ag[i][6], ag[i][7]);
+      pb[0] = make_float4(ab[i][0], ab[i][1], ab[i][2], ab[i][3]);
+      pb[1] = make_float4(ab[i][4], ab[i][5], ab[i][6], ab[i][7]);
+    }
+  }
+  if (w == LN5_CONSUMERS) __syncthreads();  // (A) for the producer warp
+  __syncthreads();                          // (B) partials written
+  if (n > 0) {
+    const float* red = reinterpret_cast<const float*>(smem);
+    for (int c = threadIdx.x; c < h; c += LN5_THREADS) {
+      float tg = 0.f, tb = 0.f;
+#pragma unroll
+      for (int q = 0; q < LN5_CONSUMERS; ++q) {
+        tg += red[(2 * q) * h + c];
+        tb += red[(2 * q + 1) * h + c];
+      }
+      atomicAdd(&dgain[c], tg);
+      atomicAdd(&dbias[c], tb);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) mse_loss_kernel(const __nv_bfloat16* __restrict__ z, int64_t n,
                                                         __nv_bfloat16* __restrict__ dz,
                                                         double* __restrict__ sumsq) {
@@ -601,6 +761,42 @@ cudaError_t ln_bwd_launch(const void* dy, const void* x, const float* g, const v
 #undef L3
 #undef LB
     return cudaGetLastError();
+  }
+  // v5 (ring of bulk-copied rows, whole rows per warp, fused gain / bias sums) for
+  // h <= 2048; HX_LN_BWD5=0 keeps the v1 pair for A/B runs
+  static const int v5 = getenv("HX_LN_BWD5") ? atoi(getenv("HX_LN_BWD5")) : 1;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(dy) | reinterpret_cast<uintptr_t>(x) |
+                         reinterpret_cast<uintptr_t>(dres)) & 15) == 0;
+  if (v5 && ln_version() >= 2 && h % 256 == 0 && h <= 2048 && aligned) {
+    const int smem = LN5_RING_BYTES + h * 4 + 2 * 8 * (LN5_RING_BYTES / (2 * h * 2));
+#define L5(NV)                                                                                            \
+  {                                                                                                       \
+    static bool set_##NV = false;                                                                         \
+    if (!set_##NV) {                                                                                      \
+      cudaError_t e5 = cudaFuncSetAttribute(ln_bwd_v5_kernel<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                            LN5_RING_BYTES + 2048 * 4 + 2 * 8 * (LN5_RING_BYTES / 1024));  \
+      if (e5 != cudaSuccess) return e5;                                                                   \
+      set_##NV = true;                                                                                    \
+    }                                                                                                     \
+    const int grid = rows < num_sms() ? (rows > 0 ? rows : 1) : num_sms();                                \
+    const int per = (rows + grid - 1) / grid;                                                             \
+    ln_bwd_v5_kernel<NV><<<grid, LN5_THREADS, smem, st>>>(                                                 \
+        static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x), g,                     \
+        static_cast<const __nv_bfloat16*>(dres), static_cast<__nv_bfloat16*>(dx), dg, db, rows, h, per);    \
+    return cudaGetLastError();                                                                            \
+  }
+    switch (h / 256) {
+      case 1: L5(1)
+      case 2: L5(2)
+      case 3: L5(3)
+      case 4: L5(4)
+      case 5: L5(5)
+      case 6: L5(6)
+      case 7: L5(7)
+      case 8: L5(8)
+      default: break;
+    }
+#undef L5
   }
   float2* st2 = reinterpret_cast<float2*>(stats);
 #define L(NV)                                                                                   \

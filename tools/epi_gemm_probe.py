@@ -1,7 +1,8 @@
 #!/usr/bin/env python
 """Runs the two heavy-epilogue GEMMs of the MLP once each at the GPT-1.3B/32k
 shape (W1 + GeLU writing m1 and g; W2^T + GeLU' reading m1) -- a target for
-`ncu -k regex:gemm_2sm -c 2` source-counter captures."""
+`ncu -k regex:gemm_2sm -c 2` source-counter captures.  ``--ln`` adds one
+LayerNorm backward (+ residual gradient) at T=32k, h=2048."""
 import sys
 from pathlib import Path
 
@@ -21,5 +22,11 @@ K.linear_gelu(a, w1, m1, g)
 dy = torch.randn(T, h, device=dev).to(bf)
 dm1 = torch.empty(T, 4 * h, dtype=bf, device=dev)
 K.linear_dx_dgelu(dy, w2, m1, dm1)
+if "--ln" in sys.argv:
+    x = torch.randn(T, h, device=dev).to(bf)
+    gain = torch.ones(h, device=dev)
+    dx = torch.empty_like(x)
+    dg, db = torch.zeros(h, device=dev), torch.zeros(h, device=dev)
+    K.layernorm_bwd(dy, x, gain, dy, dx, dg, db)
 torch.cuda.synchronize()
 print("ok")

@@ -522,6 +522,14 @@ __global__ void __launch_bounds__(512, 1)
       for (int it = 0; it < n_it; ++it) {
         const int st = it & 1, q0 = (kt + it) * AT_TILE;
         mbar_wait(&q_empty[st], ((it >> 1) & 1) ^ 1);
+#ifdef HX_BWD_NOQDO  // debug-only probe: no Q / dO traffic after the first two tiles (wrong results)
+        if (it >= 2) {
+          mbar_arrive(&q_full[st]);
+          mbar_wait(do_empty, (it & 1) ^ 1);
+          mbar_arrive(do_full);
+          continue;
+        }
+#endif
         mbar_arrive_expect_tx(&q_full[st], Tile<D>::BYTES);
         tma_tile_rows<D>(smem + L::Q + st * Tile<D>::BYTES, &tm_qkv, &q_full[st], qcol, bi, q0, AT_TILE);
         mbar_wait(do_empty, (it & 1) ^ 1);

@@ -165,6 +165,14 @@ HX_DEVICE uint32_t exp2_pack_poly(uint64_t x2, float& s0, float& s1) {
 // Pair i of an unrolled softmax row: every HX_POLY_EVERY-th pair on the FMA pipe.
 // (i is a compile-time constant after unrolling, so the choice costs nothing.)
 HX_DEVICE uint32_t exp2_pack_mixed(uint64_t x2, int i, float& s0, float& s1) {
+#ifdef HX_FWD_NOEXP  // debug-only probe: no exponentials at all (results wrong)
+  {
+    const float2 xu = f2unpack(x2);
+    s0 = xu.x * 0.5f;
+    s1 = xu.y * 0.5f;
+    return pack_bf16(s0, s1);
+  }
+#endif
   if constexpr (HX_POLY_EVERY > 0) {
     constexpr int every = HX_POLY_EVERY > 0 ? HX_POLY_EVERY : 1;
     if (i % every == every - 1) return exp2_pack_poly(x2, s0, s1);

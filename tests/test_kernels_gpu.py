@@ -175,7 +175,10 @@ def test_gemm_epilogues():
 
 @pytest.mark.parametrize("T,h,with_res", [(1000, 256, True), (1001, 2048, True), (1003, 2048, False),
                                            (999, 4096, True), (517, 8192, True), (300, 264, False),
-                                           (5, 512, True), (4099, 1024, False)])
+                                           (5, 512, True), (4099, 1024, False),
+                                           # backward v5 at every ring width class (h = 256 * NV,
+                                           # NV = 3, 6, 7) and fewer rows than SMs
+                                           (777, 768, True), (20000, 1536, False), (2, 1792, True)])
 def test_layernorm_fwd_bwd(T, h, with_res):
     # ragged row counts, h up to 8192 and h % 256 != 0, with and without the
     # residual gradient; dgain / dbias accumulate into their prior contents

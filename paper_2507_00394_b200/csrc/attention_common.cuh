@@ -102,33 +102,7 @@ HX_DEVICE float exp2_mixed(float x, int k) {
   return fast_exp2(x);
 }
 
-// Packed two-wide fp32 arithmetic (sm_100 FFMA2 / FADD2 / FMUL2) and the
-// three-input max (FMNMX3): half the issue slots for the softmax element math.
-HX_DEVICE uint64_t f2pack(float a, float b) {
-  uint64_t r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-  return r;
-}
-HX_DEVICE float2 f2unpack(uint64_t r) {
-  float a, b;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
-  return make_float2(a, b);
-}
-HX_DEVICE uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
-  uint64_t d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-HX_DEVICE uint64_t fadd2(uint64_t a, uint64_t b) {
-  uint64_t d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-HX_DEVICE uint64_t fmul2(uint64_t a, uint64_t b) {
-  uint64_t d;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
+// (packed two-wide fp32 helpers f2pack / ffma2 / fadd2 / fmul2: hx_common.cuh)
 HX_DEVICE float fmax3(float a, float b, float c) {
   float d;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));

@@ -113,8 +113,9 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row, int
           x[2 * i] += f.x;
           x[2 * i + 1] += f.y;
         } else {
-          x[2 * i] *= gelu_erf_grad(f.x);
-          x[2 * i + 1] *= gelu_erf_grad(f.y);
+          const float2 d = gelu_erf_grad_pair(f.x, f.y);
+          x[2 * i] *= d.x;
+          x[2 * i + 1] *= d.y;
         }
       }
     }
@@ -125,12 +126,13 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row, int
     o.w = pack_bf16(x[6], x[7]);
     *reinterpret_cast<uint4*>(out + 8 * j) = o;
     if (epi == HX_EPI_GELU) {
-      uint4 g;
-      g.x = pack_bf16(gelu_erf(x[0]), gelu_erf(x[1]));
-      g.y = pack_bf16(gelu_erf(x[2]), gelu_erf(x[3]));
-      g.z = pack_bf16(gelu_erf(x[4]), gelu_erf(x[5]));
-      g.w = pack_bf16(gelu_erf(x[6]), gelu_erf(x[7]));
-      *reinterpret_cast<uint4*>(out2 + 8 * j) = g;
+      uint32_t gw[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 t = gelu_erf_pair(x[2 * i], x[2 * i + 1]);
+        gw[i] = pack_bf16(t.x, t.y);
+      }
+      *reinterpret_cast<uint4*>(out2 + 8 * j) = make_uint4(gw[0], gw[1], gw[2], gw[3]);
     }
   }
 }
@@ -153,8 +155,9 @@ __device__ __forceinline__ void epilogue_values(int epi, const uint32_t (&acc)[3
           x[2 * i] += f.x;
           x[2 * i + 1] += f.y;
         } else {
-          x[2 * i] *= gelu_erf_grad(f.x);
-          x[2 * i + 1] *= gelu_erf_grad(f.y);
+          const float2 d = gelu_erf_grad_pair(f.x, f.y);
+          x[2 * i] *= d.x;
+          x[2 * i + 1] *= d.y;
         }
       }
     }
@@ -162,7 +165,10 @@ __device__ __forceinline__ void epilogue_values(int epi, const uint32_t (&acc)[3
     for (int i = 0; i < 4; ++i) o[4 * j + i] = pack_bf16(x[2 * i], x[2 * i + 1]);
     if (epi == HX_EPI_GELU) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) o2[4 * j + i] = pack_bf16(gelu_erf(x[2 * i]), gelu_erf(x[2 * i + 1]));
+      for (int i = 0; i < 4; ++i) {
+        const float2 t = gelu_erf_pair(x[2 * i], x[2 * i + 1]);
+        o2[4 * j + i] = pack_bf16(t.x, t.y);
+      }
     }
   }
 }

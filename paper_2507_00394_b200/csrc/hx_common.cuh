@@ -483,6 +483,33 @@ __host__ __device__ constexpr uint32_t idesc_bf16(uint32_t M, uint32_t N, bool a
 }
 
 // ---------------------------------------------------------------- math
+// Packed two-wide fp32 arithmetic (sm_100 FFMA2 / FADD2 / FMUL2) (half the
+// issue slots for element math: the attention softmax, the GeLU epilogues).
+HX_DEVICE uint64_t f2pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+HX_DEVICE float2 f2unpack(uint64_t r) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+  return make_float2(a, b);
+}
+HX_DEVICE uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+HX_DEVICE uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+HX_DEVICE uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
 // erf(x / sqrt(2)) given e = exp(-x^2 / 2): Abramowitz & Stegun 7.1.26 (|error|
 // <= 1.5e-7, the level of erff itself and far below the bf16 rounding of every
 // GeLU output), 1 reciprocal + 5 FMAs instead of erff's ~25 instructions.  The
@@ -527,12 +554,57 @@ HX_DEVICE float gelu_erf_grad(float x) {
   const float e = gauss_exp(x);
   return 0.5f * (1.0f + erf_over_sqrt2(x, e)) + x * e * 0.39894228040143268f;
 }
+
+// The same two functions on a pair of elements with FFMA2 / FMUL2 (the GEMM
+// epilogues' element math at ~10 instead of ~17 issue slots per element; the
+// epilogue warps share each SMSP with the MMA issuer or the TMA producer).
+// erf(x / sqrt2) = sign(x) * (1 - q), q = poly(t) * t * exp(-x^2 / 2).
+HX_DEVICE uint64_t erf_q_pair(uint64_t x, uint64_t& e) {
+  const float2 xf = f2unpack(x);
+  const uint64_t a = fmul2(fmul2(x, x), f2pack(-0.72134752044448170f, -0.72134752044448170f));
+  const float2 af = f2unpack(a);
+  float e0, e1;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(af.x));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(af.y));
+  e = f2pack(e0, e1);
+  const uint64_t z = fmul2(f2pack(fabsf(xf.x), fabsf(xf.y)), f2pack(0.70710678118654752f, 0.70710678118654752f));
+  const float2 den = f2unpack(ffma2(z, f2pack(0.3275911f, 0.3275911f), f2pack(1.0f, 1.0f)));
+  const uint64_t t = f2pack(rcp_approx(den.x), rcp_approx(den.y));
+  uint64_t poly = ffma2(t, f2pack(1.061405429f, 1.061405429f), f2pack(-1.453152027f, -1.453152027f));
+  poly = ffma2(poly, t, f2pack(1.421413741f, 1.421413741f));
+  poly = ffma2(poly, t, f2pack(-0.284496736f, -0.284496736f));
+  poly = ffma2(poly, t, f2pack(0.254829592f, 0.254829592f));
+  return fmul2(fmul2(poly, t), e);
+}
+// sign(x) * (1 - q) + 1 = x >= 0 ? 2 - q : q
+HX_DEVICE uint64_t one_plus_erf_pair(uint64_t x, uint64_t q) {
+  const float2 xf = f2unpack(x), qf = f2unpack(q);
+  return f2pack(xf.x >= 0.f ? 2.0f - qf.x : qf.x, xf.y >= 0.f ? 2.0f - qf.y : qf.y);
+}
+HX_DEVICE float2 gelu_erf_pair(float x0, float x1) {
+  const uint64_t x = f2pack(x0, x1);
+  uint64_t e;
+  const uint64_t q = erf_q_pair(x, e);
+  return f2unpack(fmul2(fmul2(x, f2pack(0.5f, 0.5f)), one_plus_erf_pair(x, q)));
+}
+HX_DEVICE float2 gelu_erf_grad_pair(float x0, float x1) {
+  const uint64_t x = f2pack(x0, x1);
+  uint64_t e;
+  const uint64_t q = erf_q_pair(x, e);
+  // 0.5 * (1 + erf) + x * e / sqrt(2 pi)
+  return f2unpack(ffma2(fmul2(x, e), f2pack(0.39894228040143268f, 0.39894228040143268f),
+                        fmul2(one_plus_erf_pair(x, q), f2pack(0.5f, 0.5f))));
+}
 #else  // libm erff (A/B builds: -DHX_EXACT_ERF)
 HX_DEVICE float gelu_erf(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
 
 HX_DEVICE float gelu_erf_grad(float x) {
   return 0.5f * (1.0f + erff(x * 0.70710678118654752f)) +
          x * __expf(-0.5f * x * x) * 0.39894228040143268f;
+}
+HX_DEVICE float2 gelu_erf_pair(float x0, float x1) { return make_float2(gelu_erf(x0), gelu_erf(x1)); }
+HX_DEVICE float2 gelu_erf_grad_pair(float x0, float x1) {
+  return make_float2(gelu_erf_grad(x0), gelu_erf_grad(x1));
 }
 #endif
 

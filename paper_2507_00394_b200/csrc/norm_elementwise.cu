@@ -440,12 +440,14 @@ __global__ void __launch_bounds__(256, MINB) ln_bwd_v2_kernel(
 // barrier-bound and v1 re-reads x and dy for the gain / bias sums.  Rows stream
 // through a shared-memory ring filled by 1-D bulk copies (cp.async.bulk, the
 // TMA engine) from a producer warp: each slot holds one row of x, dy (and the
-// residual gradient), so up to LN5_SLOTS rows per SM are in flight without a
-// register holding them.  Each of the 8 consumer warps owns whole rows (warp
+// residual gradient), so up to 16 rows per SM (h = 2048) are in flight without a
+// register holding them.  Each of the 7 consumer warps owns whole rows (warp
 // shuffles for the row statistics, no block barrier in the loop) and keeps its
 // lanes' gain / bias gradient partials in registers across all its rows; the
 // block combines them once at the end.  HBM traffic is the algorithmic
 // 4*T*h*2 bytes (3*T*h*2 without a residual gradient), each row read once.
+// 7 consumers + the producer = 8 warps, so the per-SMSP register file allows 255
+// registers (9 warps capped ptxas at 168 and spilled the 128 gradient partials).
 constexpr int LN5_CONSUMERS = 7;
 constexpr int LN5_THREADS = 32 * (LN5_CONSUMERS + 1);
 constexpr int LN5_RING_BYTES = 192 * 1024;

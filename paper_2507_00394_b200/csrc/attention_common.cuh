@@ -126,7 +126,9 @@ HX_DEVICE uint32_t exp2_pack_poly(uint64_t x2, float& s0, float& s1) {
   const uint64_t x = f2pack(fmaxf(xu.x, -125.f), fmaxf(xu.y, -125.f));
   constexpr float MAGIC = 12582912.f;
   const uint64_t j = fadd2(x, f2pack(MAGIC, MAGIC));
-  const uint64_t f = fadd2(x, fadd2(f2pack(MAGIC, MAGIC), j ^ 0x8000000080000000ull));
+  // f = x - n with n = j - MAGIC (exact): one FADD2 + one FFMA2 (was two FADD2 and
+  // two LOP3 sign flips)
+  const uint64_t f = ffma2(fadd2(j, f2pack(-MAGIC, -MAGIC)), f2pack(-1.f, -1.f), x);
   uint64_t q = ffma2(f, f2pack(0.0551716536f, 0.0551716536f), f2pack(0.242611155f, 0.242611155f));
   q = ffma2(f, q, f2pack(0.693260968f, 0.693260968f));
   q = ffma2(f, q, f2pack(0.999928057f, 0.999928057f));

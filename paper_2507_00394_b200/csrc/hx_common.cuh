@@ -510,54 +510,24 @@ HX_DEVICE uint64_t fmul2(uint64_t a, uint64_t b) {
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
 }
-// erf(x / sqrt(2)) given e = exp(-x^2 / 2): Abramowitz & Stegun 7.1.26 (|error|
-// <= 1.5e-7, the level of erff itself and far below the bf16 rounding of every
-// GeLU output), 1 reciprocal + 5 FMAs instead of erff's ~25 instructions.  The
-// GeLU-gradient epilogue shares e with its density term.  The reciprocal is the
-// bare MUFU.RCP (its argument is >= 1, so approx/ftz lose nothing the 1.5e-7
-// bound does not already allow): __frcp_rn wrapped every element in a
-// special-case branch and a CALL to its slow path (131 CALL / 145 BSSY in the
-// GEMM's SASS), ~2x the epilogue's instruction count.
 HX_DEVICE float rcp_approx(float x) {
   float r;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
 
-HX_DEVICE float erf_over_sqrt2(float x, float e) {
-  const float z = fabsf(x) * 0.70710678118654752f;
-  const float t = rcp_approx(fmaf(0.3275911f, z, 1.0f));
-  float poly = fmaf(1.061405429f, t, -1.453152027f);
-  poly = fmaf(poly, t, 1.421413741f);
-  poly = fmaf(poly, t, -0.284496736f);
-  poly = fmaf(poly, t, 0.254829592f);
-  const float r = fmaf(-poly * t, e, 1.0f);
-  return copysignf(r, x);
-}
-
 #ifndef HX_EXACT_ERF
-// exp(-x^2 / 2) as one bare MUFU.EX2 (ftz: __expf's denormal guard cost an
-// FSETP and two predicated FMULs per element; results below 2^-126 only feed
-// terms far under the bf16 rounding of the outputs)
-HX_DEVICE float gauss_exp(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(-0.72134752044448170f * x * x));
-  return y;
-}
-
-HX_DEVICE float gelu_erf(float x) {
-  const float e = gauss_exp(x);
-  return 0.5f * x * (1.0f + erf_over_sqrt2(x, e));
-}
-
-HX_DEVICE float gelu_erf_grad(float x) {
-  const float e = gauss_exp(x);
-  return 0.5f * (1.0f + erf_over_sqrt2(x, e)) + x * e * 0.39894228040143268f;
-}
-
-// The same two functions on a pair of elements with FFMA2 / FMUL2 (the GEMM
-// epilogues' element math at ~10 instead of ~17 issue slots per element; the
-// epilogue warps share each SMSP with the MMA issuer or the TMA producer).
+// GeLU (exact-erf form, P/runtime/mathops.py) and its derivative for the GEMM
+// epilogues, on pairs of elements with FFMA2 / FMUL2 (~10 instead of ~17 issue
+// slots per element; the epilogue warps share each SMSP with the MMA issuer or
+// the TMA producer).  erf(x / sqrt2) by Abramowitz & Stegun 7.1.26 (|error| <=
+// 1.5e-7, the level of erff itself and far below the bf16 rounding of every
+// output) given e = exp(-x^2 / 2), which the derivative's density term shares.
+// The exponential and the reciprocal are the bare MUFU instructions
+// (ex2 / rcp .approx.ftz: the rcp argument is >= 1): __frcp_rn wrapped every
+// element in a special-case branch and a CALL to its slow path (131 CALL / 145
+// BSSY in the GEMM's SASS) and __expf added a denormal guard, ~2x the
+// epilogue's instruction count.
 // erf(x / sqrt2) = sign(x) * (1 - q), q = poly(t) * t * exp(-x^2 / 2).
 HX_DEVICE uint64_t erf_q_pair(uint64_t x, uint64_t& e) {
   const float2 xf = f2unpack(x);

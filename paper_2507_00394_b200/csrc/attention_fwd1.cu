@@ -96,6 +96,12 @@ __global__ void __launch_bounds__(F1_THREADS, 1)
       for (int n = 0; n < 2 * nkv; ++n) {
         const int sl = n % NS;
         mbar_wait_nohint(&kv_empty[sl], ((n / NS) & 1) ^ 1);
+#ifdef HX_FWD_NOKV  // debug-only probe: no K/V traffic after the ring's first fill (wrong results)
+        if (n >= NS) {
+          mbar_arrive(&kv_full[sl]);
+          continue;
+        }
+#endif
         mbar_arrive_expect_tx(&kv_full[sl], Tile<D>::BYTES);
         tma_tile_rows<D>(slot_addr(n), &tm_qkv, &kv_full[sl], (n & 1) ? vcol : kcol, bi, (n >> 1) * AT_TILE,
                          AT_TILE);
